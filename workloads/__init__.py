@@ -1,0 +1,294 @@
+"""Seeded synthetic input generators shared by the oracle side and the CUDA side.
+
+This module holds NO arithmetic of the method (no gate application, no Kraus
+sampling, no lower bounds, no fusion, no sampling).  It only builds the
+*inputs*: circuits as ordered moments of operations, each operation carrying
+its explicit matrix (gates) or Kraus list (channels), plus readout error
+tables and observable lists.  Both `oracle/` and `paper_2111_02396_b200/`
+consume what is built here; neither imports the other.
+
+Conventions:
+  * qubit q <-> amplitude index bit q (R1);
+  * every matrix is given in Kronecker order of the listed qubits, i.e.
+    qubits[0] is the most significant matrix-index bit (R2);
+  * canonical linear op order = moments in order, ops in listed order (R5).
+
+Recipes follow SURVEY.md 8(d); seeds: circuit/calibration seed 0x211102396 + c,
+trajectory seed 0x023962111 + c for config c (1-based).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import gates
+from . import channels
+
+__all__ = [
+    "Gate", "Channel", "Circuit", "flatten", "gates", "channels",
+    "ghz4_depolarized", "sycamore_grid_qcs", "low_noise_grid", "random_circuit",
+    "circuit_seed", "trajectory_seed", "haar_unitary",
+]
+
+
+def circuit_seed(config: int) -> int:
+    return 0x211102396 + config
+
+
+def trajectory_seed(config: int) -> int:
+    return 0x023962111 + config
+
+
+@dataclass
+class Gate:
+    qubits: tuple
+    matrix: np.ndarray  # (2^q, 2^q) complex128, Kronecker order of qubits
+    name: str = "U"
+
+
+@dataclass
+class Channel:
+    qubits: tuple
+    kraus: List[np.ndarray]  # list of (2^q, 2^q) complex128, Kronecker order
+    name: str = "kraus"
+    record: bool = True
+
+
+@dataclass
+class Circuit:
+    n_qubits: int
+    moments: List[list] = field(default_factory=list)
+    p00: Optional[np.ndarray] = None  # readout: |0> read as 1
+    p11: Optional[np.ndarray] = None  # readout: |1> read as 0
+    observables: List[str] = field(default_factory=list)  # 'IXYZ' strings, char q = qubit q
+
+    def ops(self):
+        for m in self.moments:
+            for op in m:
+                yield op
+
+    @property
+    def n_channels(self) -> int:
+        return sum(isinstance(op, Channel) for op in self.ops())
+
+    @property
+    def n_gates(self) -> int:
+        return sum(isinstance(op, Gate) for op in self.ops())
+
+
+def flatten(c: Circuit):
+    """Serialize a circuit into flat arrays in canonical order (no arithmetic).
+
+    Returns dict with kind (0 gate / 1 channel), nq, qubits (n_ops x 6, -1 pad),
+    n_kraus, record, mat_off (complex offsets), mats (interleaved float64).
+    """
+    kind, nq, qubits, n_kraus, record, mat_off = [], [], [], [], [], []
+    blobs = []
+    off = 0
+    for op in c.ops():
+        q = list(op.qubits)
+        qubits.append(q + [-1] * (6 - len(q)))
+        nq.append(len(q))
+        mat_off.append(off)
+        if isinstance(op, Gate):
+            kind.append(0)
+            n_kraus.append(0)
+            record.append(0)
+            m = np.ascontiguousarray(op.matrix, dtype=np.complex128)
+            blobs.append(m.reshape(-1))
+            off += m.size
+        else:
+            kind.append(1)
+            n_kraus.append(len(op.kraus))
+            record.append(1 if op.record else 0)
+            for k in op.kraus:
+                m = np.ascontiguousarray(k, dtype=np.complex128)
+                blobs.append(m.reshape(-1))
+                off += m.size
+    mats = np.concatenate(blobs) if blobs else np.zeros(0, np.complex128)
+    return dict(
+        n=c.n_qubits,
+        kind=np.asarray(kind, np.int32),
+        nq=np.asarray(nq, np.int32),
+        qubits=np.asarray(qubits, np.int32).reshape(-1, 6),
+        n_kraus=np.asarray(n_kraus, np.int32),
+        record=np.asarray(record, np.int32),
+        mat_off=np.asarray(mat_off, np.int64),
+        mats=np.ascontiguousarray(mats.view(np.float64)),
+    )
+
+
+def haar_unitary(rng: np.random.Generator, d: int) -> np.ndarray:
+    z = (rng.standard_normal((d, d)) + 1j * rng.standard_normal((d, d))) / np.sqrt(2)
+    q, r = np.linalg.qr(z)
+    ph = np.diag(r) / np.abs(np.diag(r))
+    return q * ph[None, :]
+
+
+# ---------------------------------------------------------------------------
+# C1: GHZ-4 + depolarize(0.01) after each gate on each touched qubit.
+# ---------------------------------------------------------------------------
+def ghz4_depolarized(p: float = 0.01) -> Circuit:
+    c = Circuit(4)
+    H = gates.H()
+    CX = gates.CNOT()
+    seq = [(H, (0,)), (CX, (0, 1)), (CX, (1, 2)), (CX, (2, 3))]
+    for m, qs in seq:
+        c.moments.append([Gate(qs, m, "H" if len(qs) == 1 else "CX")])
+        c.moments.append([Channel((q,), channels.depolarize(p), "depolarize") for q in qs])
+    c.observables = ["ZIII", "IZII", "IIZI", "IIIZ", "ZZZZ", "XXXX"]
+    return c
+
+
+# ---------------------------------------------------------------------------
+# Sycamore-style grid circuits.
+# ---------------------------------------------------------------------------
+def _grid_couplers(rows: int, cols: int):
+    """Coupler patterns A/B/C/D on a rows x cols grid (qubit = r*cols + c).
+
+    A/B: horizontal pairs starting at even/odd columns; C/D: vertical pairs
+    starting at even/odd rows.  (Public Sycamore-like convention; external to
+    the paper, which only gives fSim.)"""
+    pat = {"A": [], "B": [], "C": [], "D": []}
+    for r in range(rows):
+        for c0 in range(cols - 1):
+            (pat["A"] if c0 % 2 == 0 else pat["B"]).append((r * cols + c0, r * cols + c0 + 1))
+    for r0 in range(rows - 1):
+        for c in range(cols):
+            (pat["C"] if r0 % 2 == 0 else pat["D"]).append((r0 * cols + c, (r0 + 1) * cols + c))
+    return pat
+
+
+def sycamore_grid_qcs(rows: int = 4, cols: int = 5, cycles: int = 14,
+                      config: int = 2, noise: bool = True,
+                      depol_1q: float = 1e-3, depol_2q: float = 5e-3,
+                      t1q_ns: float = 25.0, t2q_ns: float = 32.0) -> Circuit:
+    """C2: Sycamore-style random circuit with the approximate QCS noise model.
+
+    Per cycle: 1q layer {sqrtX, sqrtY, sqrtW} (never repeating on a qubit),
+    depolarizing(r=1e-3) after each 1q gate, decay/dephasing triple on every
+    qubit (t = 25 ns); fSim(pi/2, pi/6) on pattern ABCDCDAB, coherent error
+    fSim(dtheta, dphi) after it, 2q depolarizing (r=5e-3), decay triple on every
+    qubit (t = 32 ns).  Calibration: T1 ~ U[12,20] us, Tphi ~ U[20,40] us,
+    p00 ~ U[0.005,0.015], p11 ~ U[0.03,0.06], dtheta,dphi ~ N(0, 0.02) per pair.
+    These are synthetic typical-order values, not the paper's.
+    """
+    rng = np.random.default_rng(circuit_seed(config))
+    n = rows * cols
+    c = Circuit(n)
+    T1 = rng.uniform(12e3, 20e3, n)      # ns
+    Tphi = rng.uniform(20e3, 40e3, n)    # ns
+    c.p00 = rng.uniform(0.005, 0.015, n) if noise else None
+    c.p11 = rng.uniform(0.03, 0.06, n) if noise else None
+    pats = _grid_couplers(rows, cols)
+    pair_err = {}
+    for name in "ABCD":
+        for pr in pats[name]:
+            pair_err[pr] = (rng.normal(0, 0.02), rng.normal(0, 0.02))
+    one_q = [gates.sqrt_x(), gates.sqrt_y(), gates.sqrt_w()]
+    prev = [-1] * n
+    order = "ABCDCDAB"
+    fsim = gates.fsim(np.pi / 2, np.pi / 6)
+    for cyc in range(cycles):
+        m1 = []
+        for q in range(n):
+            choices = [i for i in range(3) if i != prev[q]]
+            k = choices[rng.integers(len(choices))]
+            prev[q] = k
+            m1.append(Gate((q,), one_q[k], ["sqrtX", "sqrtY", "sqrtW"][k]))
+        c.moments.append(m1)
+        if noise:
+            c.moments.append([Channel((q,), channels.depolarize(depol_1q), "depolarize") for q in range(n)])
+            c.moments.append([Channel((q,), channels.decay_dephase(t1q_ns, T1[q], Tphi[q]), "decay")
+                              for q in range(n)])
+        pairs = pats[order[cyc % len(order)]]
+        c.moments.append([Gate(pr, fsim, "fSim") for pr in pairs])
+        if noise:
+            c.moments.append([Gate(pr, gates.fsim(*pair_err[pr]), "fSim_err") for pr in pairs])
+            c.moments.append([Channel(pr, channels.depolarize2(depol_2q), "depolarize2") for pr in pairs])
+            c.moments.append([Channel((q,), channels.decay_dephase(t2q_ns, T1[q], Tphi[q]), "decay")
+                              for q in range(n)])
+    c.observables = ["I" * q + "Z" + "I" * (n - q - 1) for q in range(n)]
+    return c
+
+
+def low_noise_grid(rows: int = 2, cols: int = 13, cycles: int = 20, config: int = 3,
+                   depol: float = 1e-3, gamma_pd: float = 1e-4) -> Circuit:
+    """C3: depolarize(1e-3) after every gate (unitary mixture, always deferred)
+    plus phase_damp(gamma) on every qubit per moment."""
+    rng = np.random.default_rng(circuit_seed(config))
+    n = rows * cols
+    c = Circuit(n)
+    pats = _grid_couplers(rows, cols)
+    one_q = [gates.sqrt_x(), gates.sqrt_y(), gates.sqrt_w()]
+    prev = [-1] * n
+    order = "ABCDCDAB"
+    fsim = gates.fsim(np.pi / 2, np.pi / 6)
+    for cyc in range(cycles):
+        m1 = []
+        for q in range(n):
+            choices = [i for i in range(3) if i != prev[q]]
+            k = choices[rng.integers(len(choices))]
+            prev[q] = k
+            m1.append(Gate((q,), one_q[k]))
+        c.moments.append(m1)
+        c.moments.append([Channel((q,), channels.depolarize(depol)) for q in range(n)])
+        c.moments.append([Channel((q,), channels.phase_damp(gamma_pd)) for q in range(n)])
+        pairs = pats[order[cyc % len(order)]]
+        c.moments.append([Gate(pr, fsim, "fSim") for pr in pairs])
+        c.moments.append([Channel(pr, channels.depolarize2(depol)) for pr in pairs])
+        c.moments.append([Channel((q,), channels.phase_damp(gamma_pd)) for q in range(n)])
+    c.observables = ["I" * q + "Z" + "I" * (n - q - 1) for q in range(n)]
+    return c
+
+
+def random_circuit(n: int, depth: int, seed: int, max_arity: int = 2,
+                   noise: Optional[str] = None, p: float = 0.01,
+                   t1_ns: float = 3000.0, tphi_ns: float = 6000.0,
+                   t_ns: float = 32.0, readout: bool = False) -> Circuit:
+    """Haar-random 1q/2q (up to max_arity) gates on random disjoint qubits.
+
+    noise: None | 'depol' | 'decay' | 'both' | 'ad' (amplitude damping p) |
+    'pd' (phase damping p) -- channels after every gate on its qubits."""
+    rng = np.random.default_rng(seed)
+    c = Circuit(n)
+    for _ in range(depth):
+        perm = list(rng.permutation(n))
+        moment, nmoment = [], []
+        while perm:
+            k = int(rng.integers(1, max_arity + 1))
+            k = min(k, len(perm))
+            qs = tuple(int(x) for x in perm[:k])
+            perm = perm[k:]
+            moment.append(Gate(qs, haar_unitary(rng, 2 ** k)))
+            if noise is not None:
+                for q in qs:
+                    if noise in ("depol", "both"):
+                        nmoment.append(Channel((q,), channels.depolarize(p)))
+                    if noise in ("decay", "both"):
+                        nmoment.append(Channel((q,), channels.decay_dephase(t_ns, t1_ns, tphi_ns)))
+                    if noise == "ad":
+                        nmoment.append(Channel((q,), channels.amplitude_damp(p)))
+                    if noise == "pd":
+                        nmoment.append(Channel((q,), channels.phase_damp(p)))
+        c.moments.append(moment)
+        if nmoment:
+            # channels on the same qubit would collide inside one moment;
+            # split into as many moments as needed (order preserved)
+            while nmoment:
+                used, cur, rest = set(), [], []
+                for ch in nmoment:
+                    if used.isdisjoint(ch.qubits):
+                        cur.append(ch)
+                        used.update(ch.qubits)
+                    else:
+                        rest.append(ch)
+                c.moments.append(cur)
+                nmoment = rest
+    if readout:
+        c.p00 = rng.uniform(0.005, 0.015, n)
+        c.p11 = rng.uniform(0.03, 0.06, n)
+    c.observables = ["I" * q + "Z" + "I" * (n - q - 1) for q in range(n)]
+    return c
