@@ -1,0 +1,331 @@
+"""bench.py -- noisy trajectories/s of config 2 (BASELINE.json configs[1]).
+
+Workload: 20-qubit Sycamore-style random circuit, 14 cycles,
+approximate QCS noise model (decay/dephasing triple on every qubit after every
+moment, 1q/2q depolarizing after gates, fSim coherent errors, readout errors),
+10^4 trajectories per step split over N ranks (trajectory t on rank t mod N),
+1 shot per trajectory + <Z_q> for every qubit.  Synthetic, seeded inputs.
+
+A step = one pass of the whole hot path over the 10^4 trajectories: Alg. 2
+draws + delayed-inner-product classification + fusion (host, overlapped),
+fused tile passes with on-device rho_Q/choose (K1/K2), block sums,
+observables (K4), chain-rule sampling + readout (K3), records to the host.
+Strong scaling: the total (10^4) is fixed as N grows.
+
+`python bench.py --impl reference` times the CPU oracle (plain fp64 C, one
+trajectory per host core) on the same workload: the reference arm of this tier.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+CONFIG = 2
+TOTAL_TRAJ = 10_000
+N_QUBITS = 20
+METRIC = "noisy trajectories/s (C2: 20q Sycamore-style depth-14, approximate QCS noise)"
+UNIT = "trajectories/s"
+CLOCK_QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={CLOCK_QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, nm in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def rank_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def my_share(rank, world):
+    count = (TOTAL_TRAJ - rank + world - 1) // world
+    return rank, world, count  # traj_begin, stride, count
+
+
+def run_oracle_sample(circ, seed, count, begin, stride, threads):
+    import oracle
+    t0 = time.perf_counter()
+    r = oracle.run_trajectories(circ, seed=seed, traj_begin=begin, stride=stride, traj_count=count, shots=1,
+                                threads=threads)
+    dt = time.perf_counter() - t0
+    assert r["rc"] == 0
+    return dt
+
+
+def bench_reference(args):
+    rank, world, _ = rank_env()
+    if rank != 0:
+        return  # rank 0 alone runs the CPU oracle
+    circ = workloads.sycamore_grid_qcs(config=CONFIG)
+    seed = workloads.trajectory_seed(CONFIG)
+    cores = os.cpu_count() or 1
+    per_step = cores  # one trajectory per host core per step (bounded sample)
+    for w in range(args.warmup):
+        run_oracle_sample(circ, seed, per_step, w * 97, 1009, cores)
+    tot = 0.0
+    for s in range(args.steps):
+        tot += run_oracle_sample(circ, seed, per_step, 13 + s * 131, 997, cores)
+    value = per_step * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded C2 generator)",
+        "config": {"workload": "C2 20q sycamore-grid depth14 QCS-noise", "trajectories_per_step": per_step,
+                   "l2": "n/a (CPU)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{per_step} trajectory indices per step, one per core, plain fp64 C oracle"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def build_plan(circ, f):
+    from paper_2111_02396_b200 import qtraj
+    c = qtraj.Circuit.from_description(circ)
+    return c, qtraj.Plan(c, max_fused=f)
+
+
+def circuit_bytes(circ):
+    b = 0
+    for op in circ.ops():
+        if hasattr(op, "kraus"):
+            b += sum(np.asarray(k).size * 16 for k in op.kraus)
+        else:
+            b += np.asarray(op.matrix).size * 16
+    return b + 2 * 8 * circ.n_qubits
+
+
+def bench_gpu(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2111_02396_b200 import qtraj
+    rank, world, local = rank_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    circ = workloads.sycamore_grid_qcs(config=CONFIG)
+    seed = workloads.trajectory_seed(CONFIG)
+    obs = circ.observables
+    begin, stride, count = my_share(rank, world)
+    ctx = qtraj.Context(local)
+    _, plan = build_plan(circ, args.fuse)
+    batch = args.batch
+    state = torch.empty(batch << N_QUBITS, dtype=torch.complex64, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def step(profile):
+        out = ctx.run_trajectories(plan, state, seed=seed, traj_count=count, traj_begin=begin, traj_stride=stride,
+                                   shots=1, batch=batch, observables=obs, profile=profile)
+        # job output: per-observable sums over this rank's trajectories, reduced over ranks
+        sums = torch.tensor(np.concatenate([out["obs"].sum(0), (out["obs"] ** 2).sum(0)]), device=dev,
+                            dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(sums)
+        return out, sums
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    times, stats = [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)  # L2 flush between timed steps (outside the events)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            out, sums = step(True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            stats.append(out["stats"])
+    tot_ms = float(np.sum(times))
+    t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot_ms = float(t.item())
+    value = TOTAL_TRAJ * args.steps / (tot_ms / 1e3)
+
+    # ---- e2e: host circuit arrays -> C ABI (upload, fuse, run) -> host results
+    e2e_times = []
+    for _ in range(max(1, min(args.steps, 2))):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        c2, plan2 = build_plan(circ, args.fuse)
+        o2 = ctx.run_trajectories(plan2, state, seed=seed, traj_count=count, traj_begin=begin, traj_stride=stride,
+                                  shots=1, batch=batch, observables=obs)
+        mean = o2["obs"].mean(0)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_times.append(e0.elapsed_time(e1))
+        del c2, plan2, mean
+    te = torch.tensor([float(np.mean(e2e_times))], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = TOTAL_TRAJ / (float(te.item()) / 1e3)
+    st0 = stats[-1]
+    h2d = circuit_bytes(circ) + st0["h2d_bytes"]  # circuit upload + plan tables + trajectory programs
+    d2h = st0["d2h_bytes"]                        # bitstrings, Kraus records, observables, status
+
+    # ---- roofline of the dominant kernel (tile pass), from the timed steps
+    peaks, peak_src = load_peaks()
+    pass_ms = sum(s["pass_kernel_ms"] for s in stats)
+    pass_launches = sum(s["pass_launches"] for s in stats)
+    alg_bytes = sum(s["alg_bytes"] for s in stats)
+    alg_flops = sum(s["alg_flops"] for s in stats)
+    achieved_gbs = alg_bytes / (pass_ms / 1e3) / 1e9
+    achieved_tf = alg_flops / (pass_ms / 1e3) / 1e12
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    clocks = clk.summary()
+    mhz = clocks["sm_mhz"] or float(peaks.get("clocks_under_load", {}).get("sm_mhz_median", 1320.0))
+    fp32_peak_tf = 148 * 128 * 2 * mhz * 1e6 / 1e12  # B200: 148 SMs x 128 FP32 lanes x FMA, at the sampled clock
+    frac_hbm = achieved_gbs / hbm_peak
+    frac_alu = achieved_tf / fp32_peak_tf
+    if frac_alu > frac_hbm:
+        roof = {"bound": "alu", "achieved": achieved_tf, "peak": fp32_peak_tf, "unit": "TFLOP/s",
+                "frac": frac_alu, "traffic": None,
+                "peak_source": f"derived: 148 SM x 128 FP32 lanes x 2 flop x {mhz:.0f} MHz (sampled)",
+                "hbm": {"achieved_gbs": achieved_gbs, "peak_gbs": hbm_peak, "frac": frac_hbm,
+                        "peak_source": peak_src}}
+    else:
+        roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": frac_hbm,
+                "traffic": None, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
+                "alu": {"achieved_tflops": achieved_tf, "peak_tflops": fp32_peak_tf, "frac": frac_alu}}
+    roof["kernel"] = "tile_pass_kernel<12,4>"
+    roof["launches_timed"] = int(pass_launches)
+    roof["avg_launch_ms"] = pass_ms / max(pass_launches, 1)
+    roof["share_of_step"] = pass_ms / tot_ms if tot_ms else None
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only, bounded sample)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        dt = run_oracle_sample(circ, seed, cores, 17, 613, cores)
+        cpu = {"value": cores / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{cores} C2 trajectory indices (17 + 613 j), one per host core, fp64 C oracle, {dt:.1f} s"}
+    if rank == 0:
+        st = {k: float(np.mean([s[k] for s in stats])) for k in stats[0]}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32 (complex64 state; fp64 reductions)",
+            "data": "synthetic (seeded C2 generator; SURVEY 8(d))",
+            "config": {"workload": "C2 20q sycamore-grid depth14 QCS-noise", "trajectories_per_step": TOTAL_TRAJ,
+                       "n_qubits": N_QUBITS, "max_fused": args.fuse, "tile_bits": 12, "batch": batch,
+                       "shots_per_traj": 1, "observables": len(obs), "parallelism": f"traj{world}",
+                       "l2": "flushed between timed steps (512 MB write)"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(sum(s["launches"] for s in stats)),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "per_step_stats": {"passes_per_traj": st["passes"] / max(st["trajectories"], 1),
+                               "fused_gates_per_traj": st["fused_gates"] / max(st["trajectories"], 1),
+                               "reductions_per_traj": st["reductions"] / max(st["trajectories"], 1),
+                               "deferral_fraction": st["channels_deferred"] / max(
+                                   st["channels_deferred"] + st["channels_conventional"], 1),
+                               "plan_ms": st["plan_ms"], "device_ms": st["device_ms"],
+                               "pass_kernel_ms": st["pass_kernel_ms"]},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--fuse", type=int, default=4)
+    ap.add_argument("--batch", type=int, default=128)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,205 @@
+/*
+ * qtraj.h -- C ABI of libqtraj, the B200 (sm_100a) noisy quantum-trajectory
+ * hot path of arXiv 2111.02396 (qsim + Cirq approximate-noise simulation).
+ *
+ * Citations: P:N = PAPER.md line N (section / algorithm given alongside).
+ *
+ * Problem statement (Sec. II; Sec. III.E):
+ *   A circuit is an ordered list of moments; a moment holds operations on
+ *   disjoint qubits.  An operation is a unitary gate or a quantum
+ *   channel given by its Kraus operators {K_i}.  A quantum
+ *   trajectory picks one K_i per channel with probability
+ *   p_i = <Psi|K_i^dag K_i|Psi>, using the delayed-inner-product
+ *   sampler of Alg. 2: lower bounds pbar_i = sigma_min(K_i)^2,
+ *   s = sum pbar_i; a uniform r < s picks by the bounds and defers the
+ *   operator into gate fusion (Sec. III.B); otherwise all pending
+ *   operators are applied and p_i is computed.
+ *
+ * Conventions:
+ *   - qubit q <-> amplitude-index bit q (qubit 0 has stride 1).  State is
+ *     complex64, interleaved (re, im), 8 * 2^n bytes.
+ *   - every matrix argument is complex128, row-major, interleaved (re, im),
+ *     of size 2^nq x 2^nq, in KRONECKER order of the listed qubits:
+ *     qubits[0] is the most significant matrix-index bit.
+ *   - canonical op order: moments ascending, then call order within a moment.
+ *   - bitstrings are uint64 with bit q = qubit q (n <= 63).
+ *   - RNG: Philox4x32-10, key = (seed_lo32, seed_hi32), counter =
+ *     (ordinal, purpose, traj_lo32, traj_hi32); purpose 1 = channel draw
+ *     (ordinal = channel ordinal), 2 = sample, 3 = readout (ordinal =
+ *     shot*ceil(n/2) + level/2, half level%2).  Results are a pure function of
+ *     (circuit, plan options, seed, trajectory index): independent of batch
+ *     size, stream and GPU count.
+ *
+ * Ownership: inputs are copied at call time.  Handles are library-owned and
+ * freed by *_destroy.  State buffers are CALLER-OWNED device memory (e.g. a
+ * torch tensor) used on the caller's stream; the library never frees them.
+ * Host outputs go into caller-allocated arrays.
+ *
+ * Errors: functions return a qt_status; negative = failure, with a message
+ * available from qt_last_error() (thread-local).  Nothing aborts.
+ * The library never falls back to a CPU implementation: without a usable
+ * CUDA device every device entry point returns QT_ECUDA.
+ */
+#ifndef QTRAJ_H
+#define QTRAJ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    QT_OK = 0,
+    QT_EINVAL = -1,       /* bad argument (null pointer, size, option) */
+    QT_EQUBIT = -2,       /* qubit out of range, or duplicated in one moment */
+    QT_EARITY = -3,       /* nq > 6, or max_fused outside [2, 6] */
+    QT_ENONUNITARY = -4,  /* gate: ||U^dag U - I||_max >= 1e-9 */
+    QT_ENONCPTP = -5,     /* channel: ||sum K^dag K - I||_max >= 1e-9 */
+    QT_EOOM = -6,         /* device or host allocation failed / buffer too small */
+    QT_ECUDA = -7,        /* CUDA runtime error or no device */
+    QT_ENCCL = -8,        /* reserved for the multi-GPU layer */
+    QT_ELEAK = -9,        /* Alg. 2 second loop fell through with residual > 1e-6 */
+    QT_ESTATE = -10       /* zero-norm state */
+} qt_status;
+
+typedef struct qt_ctx_s* qt_ctx;
+typedef struct qt_circuit_s* qt_circuit;
+typedef struct qt_plan_s* qt_plan;
+
+/* Counters of one qt_run_trajectories call (SURVEY 5 "Metrics"). */
+typedef struct {
+    uint64_t trajectories;
+    uint64_t passes;              /* tile passes executed (sum over trajectories) */
+    uint64_t fused_gates;         /* fused gates applied (sum over trajectories) */
+    uint64_t reductions;          /* rho_Q reductions = conventional channels */
+    uint64_t channels_deferred;   /* Alg. 2 first-loop picks */
+    uint64_t channels_conventional;
+    uint64_t launches;            /* kernels launched by the library */
+    double   alg_bytes;           /* algorithmic HBM bytes: 2^(n+4) per gate pass, 2^(n+3) per read-only pass */
+    double   alg_flops;           /* 2^(n+k+3) per fused k-qubit gate */
+    double   plan_ms;             /* host planning wall time */
+    double   device_ms;           /* stream time of the whole call (CUDA events) */
+    double   pass_kernel_ms;      /* sum of tile-pass kernel durations (profile mode only) */
+    uint64_t pass_launches;       /* tile-pass kernel launches timed in profile mode */
+    uint64_t h2d_bytes;           /* host->device bytes copied by the call (tables + programs) */
+    uint64_t d2h_bytes;           /* device->host bytes copied by the call (records) */
+} qt_stats;
+
+/* ---- context -------------------------------------------------------------
+ * device: CUDA ordinal; cuda_stream: a cudaStream_t (NULL = legacy default).
+ * All device work of the context is enqueued on that stream. */
+qt_status qt_ctx_create(int device, void* cuda_stream, qt_ctx* out);
+void qt_ctx_destroy(qt_ctx ctx);
+qt_status qt_ctx_set_stream(qt_ctx ctx, void* cuda_stream);
+
+/* ---- circuit upload -------------------------------------------
+ * qt_add_gate: U is 2^nq x 2^nq complex128, Kronecker order of qubits[].
+ *   Rejects non-unitary input (QT_ENONUNITARY, tolerance 1e-9).
+ * qt_add_channel: K holds n_kraus matrices of 2^nq x 2^nq, same layout, in
+ *   Kraus-list order (the order Alg. 2 iterates).  Rejects
+ *   non-trace-preserving lists (QT_ENONCPTP, 1e-9).  record != 0 makes the
+ *   chosen index appear in out_kraus of qt_run_trajectories (measurement key,
+ *   P:102).
+ * Qubits of the operations of one moment must be disjoint: QT_EQUBIT. */
+qt_status qt_circuit_create(int n_qubits, qt_circuit* out);
+void qt_circuit_destroy(qt_circuit c);
+qt_status qt_add_gate(qt_circuit c, int moment, int nq, const int* qubits, const double* U);
+qt_status qt_add_channel(qt_circuit c, int moment, int nq, const int* qubits, int n_kraus,
+                         const double* K, int record);
+/* Readout errors: p00_err[q] = probability |0> is recorded as 1,
+ * p11_err[q] = probability |1> is recorded as 0.  Either may be NULL. */
+qt_status qt_set_readout(qt_circuit c, const double* p00_err, const double* p11_err);
+/* Number of channels whose record flag is set (columns of out_kraus). */
+int qt_circuit_num_recorded(qt_circuit c);
+int qt_circuit_num_channels(qt_circuit c);
+
+/* ---- gate fuser / plan (Sec. III.B) ---------------------------
+ * max_fused = f, the paper's maximum fuse size, 2..6 (default 4).
+ * The plan snapshots the circuit, canonicalizes every matrix, precomputes the
+ * Kraus lower bounds pbar_i = sigma_min(K_i)^2 and s, and flags
+ * unitary mixtures (all K_i^dag K_i proportional to I; s = 1). */
+qt_status qt_fuse(qt_circuit c, int max_fused, qt_plan* out);
+
+typedef struct {
+    int max_fused;    /* f in [2, 6]; 0 = 4 */
+    int tile_bits;    /* qubits held per CTA tile; 0 = auto (12, or n if n < 12) */
+    int low_bits;     /* lowest qubits always in a tile (coalescing); 0 = auto (4) */
+    int one_gate_per_pass; /* 1 = every fused gate is its own HBM pass (the paper's GPU scheme) */
+} qt_fuse_opts;
+qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out);
+void qt_plan_destroy(qt_plan p);
+
+/* ---- trajectories (Alg. 2) -------------------------------------
+ * Runs trajectories t_j = traj_begin + j * traj_stride, j < traj_count,
+ * `batch` of them concurrently (batch <= state_bytes / (8 * 2^n)).
+ * state_dev: caller-owned device buffer; on return it holds the final
+ *   (unnormalized: norms are tracked lazily) states of the LAST batch,
+ *   trajectory slot b at offset b * 2^n amplitudes.
+ * out_bits : host, traj_count * shots_per_traj uint64 (after readout), or NULL.
+ * out_kraus: host, traj_count * qt_circuit_num_recorded int32 (chosen Kraus
+ *   index of each recorded channel, in canonical order), or NULL.
+ * out_obs  : host, traj_count * n_obs doubles: <psi|P|psi>/<psi|psi>, or NULL.
+ * mode: 0 = delayed inner product (Alg. 2).  Others are reserved. */
+typedef struct {
+    uint64_t seed;
+    uint64_t traj_begin;
+    uint64_t traj_stride;   /* 0 = 1 */
+    uint64_t traj_count;
+    int shots_per_traj;
+    int batch;              /* 0 = as many as the state buffer holds (max 256) */
+    int mode;
+    int profile;            /* 1 = time every tile-pass launch with CUDA events */
+    int host_threads;       /* 0 = hardware concurrency */
+} qt_run_opts;
+
+/* A Pauli string: paulis[i] in "IXYZ" acts on qubits[i]. */
+typedef struct {
+    int nq;
+    const int* qubits;
+    const char* paulis;
+} qt_pauli;
+
+qt_status qt_run_trajectories(qt_ctx ctx, qt_plan plan, const qt_run_opts* opts,
+                              int n_obs, const qt_pauli* obs,
+                              void* state_dev, size_t state_bytes,
+                              uint64_t* out_bits, int32_t* out_kraus, double* out_obs,
+                              qt_stats* out_stats);
+
+/* ---- stand-alone state operations -----------------------------------------
+ * qt_apply_gate: Alg. 1 for one gate on a caller state (in place).
+ * qt_sample_bitstrings: chain-rule sampling (most significant qubit first)
+ *   of `shots` bitstrings from |psi|^2 (norm-invariant), trajectory index
+ *   `traj` selects the RNG stream; no readout error is applied.
+ * qt_expectation_value: <psi|P|psi>/<psi|psi> for each Pauli string. */
+qt_status qt_apply_gate(qt_ctx ctx, void* state_dev, int n, int nq, const int* qubits,
+                        const double* U);
+/* qt_apply_gate_ex: as qt_apply_gate, applied `repeats` times; if kernel_ms
+ * is non-NULL it receives the mean duration of one application (CUDA events
+ * on the context stream, first application excluded as warm-up). */
+qt_status qt_apply_gate_ex(qt_ctx ctx, void* state_dev, int n, int nq, const int* qubits,
+                           const double* U, int repeats, double* kernel_ms);
+qt_status qt_sample_bitstrings(qt_ctx ctx, const void* state_dev, int n, uint64_t seed,
+                               uint64_t traj, int shots, uint64_t* out);
+qt_status qt_expectation_value(qt_ctx ctx, const void* state_dev, int n, int n_obs,
+                               const qt_pauli* obs, double* out);
+
+/* Host-only introspection of the planner (no device work): plans trajectory
+ * `traj` exactly as qt_run_trajectories would and reports
+ * out[0] tile passes, [1] fused gates, [2] conventional channels (rho_Q
+ * reductions), [3] deferred picks, [4] conventional picks, [5] matrix-pool
+ * entries, [6] algorithmic bytes, [7] fused-gate constituents. */
+qt_status qt_plan_info(qt_plan plan, uint64_t seed, uint64_t traj, int64_t* out);
+
+/* Lower bound used by the sampler, exposed for tests: sigma_min(K)^2 of a
+ * d x d complex128 matrix. */
+double qt_kraus_lower_bound(int d, const double* K);
+
+const char* qt_last_error(void);
+const char* qt_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QTRAJ_H */

@@ -1,0 +1,85 @@
+// desc.hpp -- device descriptors shared by the host planner (plan.cpp) and the
+// sm_100a kernels (kernels.cu).  Plain structs, no methods.
+#pragma once
+#include <stdint.h>
+
+namespace qt {
+
+// Pass flags.
+enum : int32_t {
+    kPassStore = 1,   // write the tile back to HBM (gate passes)
+    kPassRho = 2,     // epilogue: rho_Q partial of a conventional channel + choose
+    kPassFinal = 4,   // epilogue: block sums |psi|^2 (tile = low T qubits) for the sampler/norm
+    kPassObs = 8,     // epilogue: Pauli-string partial sums
+};
+
+// One tile pass of one trajectory (Sec. III.A Alg. 1 generalized: every CTA
+// owns the 2^T amplitudes spanned by tile_mask for one value of the other bits
+// and applies gate_count fused gates to them in shared memory / registers).
+struct PassDesc {
+    uint64_t tile_mask;   // global qubits of the tile, popcount == T
+    int32_t gate_begin;   // into GateDesc[]
+    int32_t gate_count;
+    int32_t flags;
+    int32_t event;        // EventDesc index (kPassRho) or -1
+    int32_t obs_begin;    // into ObsDesc[] (kPassObs)
+    int32_t obs_count;
+};
+
+// A fused gate inside a pass.  pos = tile-local bit positions of the gate's
+// qubits, ascending, 4 bits each (matrix bit m <-> pos m).
+struct GateDesc {
+    int32_t mat_off;      // complex64 offset into the matrix pool (16-byte aligned)
+    int32_t k;
+    uint32_t pos;
+    int32_t pad;
+};
+
+// A conventional channel occurrence (Alg. 2 lines 12-21).
+struct EventDesc {
+    int32_t chan;         // ChanDesc index
+    int32_t mat_off;      // pool slot receiving K_i / sqrt(raw p_i) (complex64)
+    int32_t record;       // index into the record array, or -1
+    int32_t slot;         // batch slot of the trajectory
+    double r;             // remaining uniform after the first loop
+};
+
+// Channel data for the device choose step (fp64 in chan_data):
+//   pbar[n_kraus], then M_i = K_i^dag K_i (2*d*d doubles each), then K_i.
+struct ChanDesc {
+    uint64_t qmask;       // global qubits of the channel
+    int32_t d;
+    int32_t n_kraus;
+    int32_t off;          // double offset into chan_data
+    int32_t nq;
+};
+
+// Fused-gate materialization: product of constituents (Sec. III.B).
+struct FusedDesc {
+    int32_t mat_off;      // complex64 pool offset
+    int32_t k;
+    int32_t cons_begin;
+    int32_t cons_count;
+};
+
+// One constituent: variant `var`, its qubits' positions inside the fused
+// gate's sorted qubit list (4 bits each), nq in bits 24..27.
+struct ConsDesc {
+    int32_t var;
+    uint32_t pos;
+};
+
+struct VarDesc {
+    int32_t off;          // complex128 offset into var_data (double2 units)
+    int32_t nq;
+};
+
+// Pauli observable: phase(L) = i^ny (-1)^popcount(L & zmask), P|L> = phase |L ^ xmask>.
+struct ObsDesc {
+    uint64_t xmask;
+    uint64_t zmask;
+    int32_t ny;
+    int32_t slot;         // column in the per-trajectory observable array
+};
+
+}  // namespace qt

@@ -1,0 +1,252 @@
+// kernels.cu -- sm_100a kernels of the noisy-trajectory hot path.
+//
+//   K1  tile_pass_kernel   Alg. 1 over a whole fused-gate program:
+//                          one CTA owns 2^T amplitudes (the qubits of
+//                          PassDesc::tile_mask, the 4 lowest always included
+//                          so HBM reads are 128-byte runs), keeps them in
+//                          shared memory, and applies every fused gate of the
+//                          pass in registers (2^R amplitudes per thread); one
+//                          shared-memory re-layout per fused gate.
+//   K2  (epilogue)         rho_Q partial sums of a conventional channel in fp64
+//                          (Alg. 2 line 14 computed in place), then the
+//                          last CTA of the trajectory reduces them in a fixed
+//                          order and walks Alg. 2 lines 13-21.
+//   K3  sample_kernel      chain-rule sampler over fp64 block sums + readout
+//                          flips.
+//   K4  (epilogue)         Pauli-string partial sums; finalize_obs_kernel.
+//   K6  materialize_kernel fused-gate matrices (Sec. III.B) built in
+//                          fp64 from their constituents, stored complex64.
+//
+// Reductions never use floating-point atomics: every sum has a fixed order
+// that depends only on n and T, so results are bit-reproducible and
+// independent of batch size and GPU count.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels.hpp"
+#include "philox.hpp"
+#include "tile_pass.cuh"
+
+namespace qt {
+
+// Tile-pass instantiations live in tile_pass_r{4,5,6}.cu (parallel compile).
+cudaError_t launch_tile_pass_r4(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s);
+cudaError_t launch_tile_pass_r5(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s);
+cudaError_t launch_tile_pass_r6(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s);
+
+size_t tile_pass_smem_bytes(int T, int R) { return tile_pass_smem_bytes_impl(T, R); }
+
+cudaError_t launch_tile_pass(const TileArgs& a, int R, int step, uint32_t ntiles, int nslots,
+                             cudaStream_t s) {
+    // Instantiated (T, R): (12, 4), (12, 5), (12, 6) and (T, min(T, 4)) for
+    // T = 1..11 (the whole state of n < 12 qubits in one CTA).
+    if (a.T == 12 && R == 6) return launch_tile_pass_r6(a, step, ntiles, nslots, s);
+    if (a.T == 12 && R == 5) return launch_tile_pass_r5(a, step, ntiles, nslots, s);
+    if (R == (a.T < 4 ? a.T : 4)) return launch_tile_pass_r4(a, step, ntiles, nslots, s);
+    return cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------------------------------
+// K6 fused-matrix materialization (fp64), one CTA per fused gate, thread c
+// builds column c: e_c pushed through the constituents in time order.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(64)
+materialize_kernel(const FusedDesc* __restrict__ fused, const ConsDesc* __restrict__ cons,
+                   const VarDesc* __restrict__ vars, const double2* __restrict__ var_data,
+                   float2* __restrict__ pool) {
+    const FusedDesc F = fused[blockIdx.x];
+    const int D = 1 << F.k;
+    const int c = threadIdx.x;
+    if (c >= D) return;
+    double2 v[64];
+    for (int i = 0; i < D; ++i) v[i] = make_double2(i == c ? 1.0 : 0.0, 0.0);
+    for (int j = 0; j < F.cons_count; ++j) {
+        const ConsDesc C = cons[F.cons_begin + j];
+        const VarDesc V = vars[C.var];
+        const int q = V.nq;
+        const int dq = 1 << q;
+        uint32_t qm = 0;
+        int pos[6];
+        for (int m = 0; m < q; ++m) {
+            pos[m] = (C.pos >> (4 * m)) & 15;
+            qm |= 1u << pos[m];
+        }
+        const double2* M = var_data + V.off;
+        for (int b0 = 0; b0 < D; ++b0) {
+            if (b0 & qm) continue;
+            double2 in[64];
+            int idx[64];
+            for (int a = 0; a < dq; ++a) {
+                int o = b0;
+                for (int m = 0; m < q; ++m)
+                    if ((a >> m) & 1) o |= 1 << pos[m];
+                idx[a] = o;
+                in[a] = v[o];
+            }
+            for (int rr = 0; rr < dq; ++rr) {
+                double re = 0.0, im = 0.0;
+                for (int a = 0; a < dq; ++a) {
+                    const double2 u = M[rr * dq + a];
+                    re += u.x * in[a].x - u.y * in[a].y;
+                    im += u.x * in[a].y + u.y * in[a].x;
+                }
+                v[idx[rr]] = make_double2(re, im);
+            }
+        }
+    }
+    for (int rr = 0; rr < D; ++rr) pool[F.mat_off + rr * D + c] = make_float2((float)v[rr].x, (float)v[rr].y);
+}
+
+cudaError_t launch_materialize(const FusedDesc* fused, int n_fused, const ConsDesc* cons,
+                               const VarDesc* vars, const double* var_data, float2* pool,
+                               cudaStream_t s) {
+    if (n_fused <= 0) return cudaSuccess;
+    materialize_kernel<<<n_fused, 64, 0, s>>>(fused, cons, vars,
+                                             reinterpret_cast<const double2*>(var_data), pool);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K4 finalize: norm = sum of block sums, obs = sum of partials / norm, in a
+// fixed order (one CTA per trajectory slot).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+finalize_obs_kernel(const double* __restrict__ blocksum, const double* __restrict__ obs_part,
+                    int ntiles, int n_obs, double* __restrict__ out_obs, double* __restrict__ out_norm) {
+    __shared__ double red[64];
+    const int slot = blockIdx.x;
+    const int tid = threadIdx.x;
+    double s = 0.0;
+    for (int t = tid; t < ntiles; t += 256) s += blocksum[(uint64_t)slot * ntiles + t];
+    const double norm = block_sum<256>(s, red);
+    if (tid == 0 && out_norm) out_norm[slot] = norm;
+    for (int o = 0; o < n_obs; ++o) {
+        double p = 0.0;
+        for (int t = tid; t < ntiles; t += 256) p += obs_part[((uint64_t)slot * ntiles + t) * n_obs + o];
+        const double tot = block_sum<256>(p, red);
+        if (tid == 0) out_obs[(uint64_t)slot * n_obs + o] = tot / norm;
+    }
+}
+
+cudaError_t launch_finalize_obs(const double* blocksum, const double* obs_part, int ntiles,
+                                int n_obs, int nslots, double* out_obs, double* out_norm,
+                                cudaStream_t s) {
+    if (nslots <= 0) return cudaSuccess;
+    finalize_obs_kernel<<<nslots, 256, 0, s>>>(blocksum, obs_part, ntiles, n_obs, out_obs, out_norm);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K3 sampler: one warp per (slot, shot).  Chain rule, most significant qubit
+// first: bit = 0 iff u * (M0 + M1) < M0; M0 == 0 -> 1; M1 == 0 -> 0.  Levels
+// n-1..T use the fp64 block sums of the contiguous 2^T-amplitude tiles, levels
+// T-1..0 read the chosen tile.  Then readout flips.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void __launch_bounds__(128)
+sample_kernel(const float2* __restrict__ state, int n, int T, const double* __restrict__ blocksum,
+              int nslots, int shots, uint64_t seed, const uint64_t* __restrict__ traj_ids,
+              const double* __restrict__ p00, const double* __restrict__ p11,
+              uint64_t* __restrict__ out_bits) {
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= nslots * shots) return;
+    const int slot = gw / shots;
+    const int shot = gw % shots;
+    const uint64_t traj = traj_ids[slot];
+    const int half_n = (n + 1) / 2;
+    const uint64_t ntiles = 1ull << (n - T);
+    const double* bs = blocksum + (uint64_t)slot * ntiles;
+    uint64_t lo = 0;  // prefix (tile index range [lo, lo + 2^(l-T+1)))
+    uint64_t bits = 0;
+    for (int l = n - 1; l >= T; --l) {
+        const uint64_t half = 1ull << (l - T);
+        double m0 = 0.0, m1 = 0.0;
+        for (uint64_t i = lane; i < half; i += 32) {
+            m0 += bs[lo + i];
+            m1 += bs[lo + half + i];
+        }
+        m0 = warp_sum(m0);
+        m1 = warp_sum(m1);
+        const double u = draw(seed, (uint32_t)(shot * half_n + l / 2), kPurposeSample, traj, l & 1);
+        int bit;
+        if (m0 == 0.0) bit = 1;
+        else if (m1 == 0.0) bit = 0;
+        else bit = (u * (m0 + m1) < m0) ? 0 : 1;
+        if (bit) {
+            lo += half;
+            bits |= 1ull << l;
+        }
+    }
+    const float2* tl = state + ((uint64_t)slot << n) + (lo << T);
+    uint32_t off = 0;
+    for (int l = T - 1; l >= 0; --l) {
+        const uint32_t half = 1u << l;
+        double m0 = 0.0, m1 = 0.0;
+        for (uint32_t i = lane; i < half; i += 32) {
+            const float2 a = tl[off + i];
+            const float2 b = tl[off + half + i];
+            m0 += (double)a.x * a.x + (double)a.y * a.y;
+            m1 += (double)b.x * b.x + (double)b.y * b.y;
+        }
+        m0 = warp_sum(m0);
+        m1 = warp_sum(m1);
+        const double u = draw(seed, (uint32_t)(shot * half_n + l / 2), kPurposeSample, traj, l & 1);
+        int bit;
+        if (m0 == 0.0) bit = 1;
+        else if (m1 == 0.0) bit = 0;
+        else bit = (u * (m0 + m1) < m0) ? 0 : 1;
+        if (bit) {
+            off += half;
+            bits |= 1ull << l;
+        }
+    }
+    if (lane == 0) {
+        uint64_t out = bits;
+        if (p00 || p11) {
+            for (int q = 0; q < n; ++q) {
+                const double u = draw(seed, (uint32_t)(shot * half_n + q / 2), kPurposeReadout, traj, q & 1);
+                const int b = (int)((bits >> q) & 1);
+                if (b == 0 && p00 && u < p00[q]) out |= 1ull << q;
+                if (b == 1 && p11 && u < p11[q]) out &= ~(1ull << q);
+            }
+        }
+        out_bits[(uint64_t)slot * shots + shot] = out;
+    }
+}
+
+cudaError_t launch_sample(const float2* state, int n, int T, const double* blocksum, int nslots,
+                          int shots, uint64_t seed, const uint64_t* traj_ids, const double* p00,
+                          const double* p11, uint64_t* out_bits, cudaStream_t s) {
+    const long warps = (long)nslots * shots;
+    if (warps <= 0) return cudaSuccess;
+    const int threads = 128;
+    const long blocks = (warps * 32 + threads - 1) / threads;
+    sample_kernel<<<(unsigned)blocks, threads, 0, s>>>(state, n, T, blocksum, nslots, shots, seed,
+                                                       traj_ids, p00, p11, out_bits);
+    return cudaGetLastError();
+}
+
+}  // namespace qt
+
+namespace qt {
+
+// |0...0> in every slot (after a memset to zero).
+__global__ void init_states_kernel(float2* state, int n, int nslots) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < nslots) state[(uint64_t)b << n] = make_float2(1.f, 0.f);
+}
+
+cudaError_t launch_init_states(float2* state, int n, int nslots, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(state, 0, sizeof(float2) * ((size_t)nslots << n), s);
+    if (e != cudaSuccess) return e;
+    init_states_kernel<<<(nslots + 127) / 128, 128, 0, s>>>(state, n, nslots);
+    return cudaGetLastError();
+}
+
+}  // namespace qt

@@ -1,0 +1,57 @@
+// kernels.hpp -- launch interface of the sm_100a kernels (kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "desc.hpp"
+
+namespace qt {
+
+// Arguments of the tile-pass kernel K1 (+ epilogues K2 rho_Q/choose, K3a block
+// sums, K4 Pauli partials).  All pointers are device pointers.
+struct TileArgs {
+    float2* state;              // batch base; slot b at offset b << n
+    int n;                      // qubits
+    int T;                      // tile bits
+    const PassDesc* passes;
+    const int32_t* pass_start;  // per slot
+    const int32_t* pass_count;  // per slot
+    const GateDesc* gates;
+    float2* pool;               // complex64 matrix pool (read by passes, written by choose)
+    const EventDesc* events;
+    const ChanDesc* chans;
+    const double* chan_data;
+    double* rho_part;           // [slot][tile][rho_stride]
+    int rho_stride;             // doubles per tile partial (2 * dmax^2)
+    int32_t* counters;          // per slot, zero-initialized
+    int32_t* records;           // chosen Kraus index of recorded channels
+    int32_t* status;            // per slot error code (0 = ok)
+    double* blocksum;           // [slot][tile]
+    double* obs_part;           // [slot][tile][n_obs]
+    int n_obs;
+    const ObsDesc* obs;
+};
+
+// Largest register width R (amplitudes per thread = 2^R) compiled.
+constexpr int kMaxR = 6;
+constexpr int kMaxT = 12;
+
+size_t tile_pass_smem_bytes(int T, int R);
+cudaError_t launch_tile_pass(const TileArgs& a, int R, int step, uint32_t ntiles, int nslots,
+                             cudaStream_t s);
+
+cudaError_t launch_materialize(const FusedDesc* fused, int n_fused, const ConsDesc* cons,
+                               const VarDesc* vars, const double* var_data, float2* pool,
+                               cudaStream_t s);
+
+cudaError_t launch_finalize_obs(const double* blocksum, const double* obs_part, int ntiles,
+                                int n_obs, int nslots, double* out_obs, double* out_norm,
+                                cudaStream_t s);
+
+cudaError_t launch_init_states(float2* state, int n, int nslots, cudaStream_t s);
+
+cudaError_t launch_sample(const float2* state, int n, int T, const double* blocksum, int nslots,
+                          int shots, uint64_t seed, const uint64_t* traj_ids, const double* p00,
+                          const double* p11, uint64_t* out_bits, cudaStream_t s);
+
+}  // namespace qt

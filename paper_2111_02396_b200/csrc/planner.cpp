@@ -1,0 +1,490 @@
+// planner.cpp -- per-trajectory program construction.
+//
+//  1. Alg. 2 first loop for every channel: one Philox draw per
+//     channel; r < cumulative pbar picks K_i and DEFERS it (it becomes an
+//     ordinary operation for the fuser); otherwise the channel is
+//     CONVENTIONAL (a barrier: every earlier operation is applied, then rho_Q
+//     is reduced on the device and lines 13-21 pick K_i there).
+//  2. Each barrier-free segment is fused with the paper's two-phase fuser
+//     (Sec. III.B) at maximum fuse size f.
+//  3. Fused gates are packed greedily into tile passes: a pass holds <= T
+//     qubits (the CL lowest always included), so one HBM read + write applies
+//     many fused gates (the B200 design; the paper applies one fused gate per
+//     sweep, which one_gate_per_pass reproduces).
+//  4. Epilogues: rho_Q at each barrier; block sums (+ Pauli partials) at the
+//     end of the trajectory.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "host.hpp"
+#include "philox.hpp"
+
+namespace qt {
+
+static inline int popc(uint64_t x) { return __builtin_popcountll(x); }
+
+// ---------------------------------------------------------------------------
+// Two-phase fuser.
+// ---------------------------------------------------------------------------
+std::vector<std::vector<int>> fuse_items(const std::vector<FuseItem>& items, int f) {
+    const int N = (int)items.size();
+    std::vector<std::vector<int>> out;
+    if (N == 0) return out;
+    int nq_max = 0;
+    for (auto& it : items) nq_max = std::max(nq_max, 64 - __builtin_clzll(it.mask | 1));
+    // per-qubit item sequences
+    std::vector<std::vector<int>> on_q(nq_max);
+    std::vector<std::array<int, 6>> slot(N);  // position of item in each of its qubits' lists
+    for (int i = 0; i < N; ++i) {
+        int m = 0;
+        for (uint64_t mk = items[i].mask; mk; mk &= mk - 1) {
+            const int q = __builtin_ctzll(mk);
+            slot[i][m++] = (int)on_q[q].size();
+            on_q[q].push_back(i);
+        }
+    }
+    auto qubit_at = [&](int i, int m) {
+        uint64_t mk = items[i].mask;
+        for (int k = 0; k < m; ++k) mk &= mk - 1;
+        return __builtin_ctzll(mk);
+    };
+    // ---- phase 1: absorb small items into time-adjacent larger ones on the same qubits
+    std::vector<int> group(N);
+    for (int i = 0; i < N; ++i) group[i] = i;
+    std::vector<int> big(N, 0);  // group anchor flags
+    auto k_of = [&](int g) { return popc(items[g].mask); };
+    std::vector<char> absorbed(N, 0);
+    // forward absorption (an item joins the next larger item on all of its qubits); reverse order
+    for (int i = N - 1; i >= 0; --i) {
+        if (items[i].fixed) continue;
+        int G = -1;
+        bool ok = true;
+        int m = 0;
+        for (uint64_t mk = items[i].mask; mk && ok; mk &= mk - 1, ++m) {
+            const int q = __builtin_ctzll(mk);
+            const int pos = slot[i][m];
+            if (pos + 1 >= (int)on_q[q].size()) { ok = false; break; }
+            const int g = group[on_q[q][pos + 1]];
+            if (G < 0) G = g;
+            else if (G != g) ok = false;
+        }
+        if (!ok || G < 0 || items[G].fixed) continue;
+        if (!((items[i].mask & ~items[G].mask) == 0 && popc(items[i].mask) < k_of(G))) continue;
+        group[i] = G;
+        absorbed[i] = 1;
+    }
+    // backward absorption of trailing small items into the previous larger item
+    std::vector<char> has_members(N, 0);
+    for (int i = 0; i < N; ++i)
+        if (group[i] != i) has_members[group[i]] = 1;
+    for (int i = 0; i < N; ++i) {
+        if (items[i].fixed || absorbed[i] || has_members[i]) continue;
+        int G = -1;
+        bool ok = true;
+        int m = 0;
+        for (uint64_t mk = items[i].mask; mk && ok; mk &= mk - 1, ++m) {
+            const int q = __builtin_ctzll(mk);
+            const int pos = slot[i][m];
+            if (pos == 0) { ok = false; break; }
+            const int g = group[on_q[q][pos - 1]];
+            if (G < 0) G = g;
+            else if (G != g) ok = false;
+        }
+        if (!ok || G < 0 || items[G].fixed) continue;
+        if (!((items[i].mask & ~items[G].mask) == 0 && popc(items[i].mask) < k_of(G))) continue;
+        group[i] = G;
+        absorbed[i] = 1;
+        has_members[G] = 1;
+    }
+    (void)big;
+    (void)qubit_at;
+    // groups: anchor id -> members (time order)
+    std::vector<int> gid(N, -1);
+    std::vector<std::vector<int>> members;
+    std::vector<uint64_t> gmask;
+    std::vector<char> gfixed;
+    for (int i = 0; i < N; ++i) {
+        const int a = group[i];
+        if (gid[a] < 0) {
+            gid[a] = (int)members.size();
+            members.emplace_back();
+            gmask.push_back(items[a].mask);
+            gfixed.push_back(items[a].fixed);
+        }
+    }
+    for (int i = 0; i < N; ++i) members[gid[group[i]]].push_back(i);
+    const int NG = (int)members.size();
+    // group order = anchor order (gid assigned in anchor order of first appearance);
+    // re-sort by anchor index to be safe
+    std::vector<int> anchor_of(NG);
+    for (int i = 0; i < N; ++i)
+        if (group[i] == i) anchor_of[gid[i]] = i;
+    std::vector<int> gorder(NG);
+    for (int g = 0; g < NG; ++g) gorder[g] = g;
+    std::sort(gorder.begin(), gorder.end(), [&](int a, int b) { return anchor_of[a] < anchor_of[b]; });
+    std::vector<int> grank(NG);
+    for (int r = 0; r < NG; ++r) grank[gorder[r]] = r;
+    // per-qubit group sequences (dedup consecutive), verify they follow rank order
+    std::vector<std::vector<int>> gq(nq_max);
+    bool valid = true;
+    for (int q = 0; q < nq_max; ++q) {
+        for (int it : on_q[q]) {
+            const int g = gid[group[it]];
+            if (gq[q].empty() || gq[q].back() != g) {
+                // strictly increasing rank also rules out non-contiguous groups
+                if (!gq[q].empty() && grank[gq[q].back()] >= grank[g]) valid = false;
+                gq[q].push_back(g);
+            }
+        }
+    }
+    if (!valid) {
+        // fall back: no phase-1 absorption
+        members.assign(N, {});
+        gmask.resize(N);
+        gfixed.resize(N);
+        for (int i = 0; i < N; ++i) {
+            members[i] = {i};
+            gmask[i] = items[i].mask;
+            gfixed[i] = items[i].fixed;
+        }
+        gorder.resize(N);
+        grank.resize(N);
+        for (int i = 0; i < N; ++i) gorder[i] = grank[i] = i;
+        for (int q = 0; q < nq_max; ++q) gq[q] = on_q[q];
+    }
+    const int G = (int)members.size();
+    // position of each group in each of its qubits' group lists
+    std::vector<std::array<int, 6>> gpos(G);
+    for (int q = 0; q < nq_max; ++q)
+        for (int k = 0; k < (int)gq[q].size(); ++k) {
+            const int g = gq[q][k];
+            int m = 0;
+            for (uint64_t mk = gmask[g]; mk; mk &= mk - 1, ++m)
+                if (__builtin_ctzll(mk) == q) gpos[g][m] = k;
+        }
+    auto pos_on = [&](int g, int q) {
+        int m = 0;
+        for (uint64_t mk = gmask[g]; mk; mk &= mk - 1, ++m)
+            if (__builtin_ctzll(mk) == q) return gpos[g][m];
+        return -1;
+    };
+    // ---- phase 2: greedy growth in increasing time order
+    std::vector<char> marked(G, 0);
+    auto ready = [&](int h) {  // all predecessors of h marked
+        for (uint64_t mk = gmask[h]; mk; mk &= mk - 1) {
+            const int q = __builtin_ctzll(mk);
+            const int p = pos_on(h, q);
+            if (p > 0 && !marked[gq[q][p - 1]]) return false;
+        }
+        return true;
+    };
+    for (int r = 0; r < G; ++r) {
+        const int g0 = gorder[r];
+        if (marked[g0]) continue;
+        std::vector<int> F{g0};
+        marked[g0] = 1;
+        uint64_t FM = gmask[g0];
+        if (!gfixed[g0]) {
+            bool added = true;
+            while (added) {
+                added = false;
+                for (uint64_t mk = FM; mk; mk &= mk - 1) {
+                    const int q = __builtin_ctzll(mk);
+                    // latest member of F on q, then the next group on q
+                    int last = -1;
+                    for (int g : F) {
+                        if (gmask[g] >> q & 1) last = std::max(last, pos_on(g, q));
+                    }
+                    if (last < 0 || last + 1 >= (int)gq[q].size()) continue;
+                    const int h = gq[q][last + 1];
+                    if (marked[h] || gfixed[h]) continue;
+                    // unmarked predecessors of h (next-nearest neighbours back in time)
+                    std::vector<int> preds;
+                    bool ok = true;
+                    uint64_t nm = FM | gmask[h];
+                    for (uint64_t hm = gmask[h]; hm && ok; hm &= hm - 1) {
+                        const int p = __builtin_ctzll(hm);
+                        const int ph = pos_on(h, p);
+                        if (ph <= 0) continue;
+                        const int pg = gq[p][ph - 1];
+                        if (marked[pg]) continue;
+                        if (gfixed[pg] || !ready(pg)) { ok = false; break; }
+                        if (std::find(preds.begin(), preds.end(), pg) == preds.end()) {
+                            preds.push_back(pg);
+                            nm |= gmask[pg];
+                        }
+                    }
+                    if (!ok || popc(nm) > f) continue;
+                    for (int pg : preds) {
+                        marked[pg] = 1;
+                        F.push_back(pg);
+                    }
+                    marked[h] = 1;
+                    F.push_back(h);
+                    FM = nm;
+                    added = true;
+                    break;  // restart from the lowest qubit with the grown set
+                }
+            }
+        }
+        std::sort(F.begin(), F.end(), [&](int a, int b) { return grank[a] < grank[b]; });
+        std::vector<int> fused_items;
+        for (int g : F)
+            for (int it : members[g]) fused_items.push_back(it);
+        out.push_back(std::move(fused_items));
+    }
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// Pass building.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct FusedGate {
+    uint64_t mask;
+    std::vector<int> items;  // indices into the segment item list
+    int special_event;       // >= 0: device-chosen conventional op (no materialization)
+};
+
+struct Item {
+    uint64_t mask;
+    int var;      // variant, or -1 for the device-chosen op
+    int event;    // event index for the device-chosen op
+    int nq;
+};
+
+inline uint64_t low_mask(int k) { return k >= 64 ? ~0ull : ((1ull << k) - 1ull); }
+
+uint64_t fill_tile(uint64_t S, int T, int n) {
+    for (int q = 0; q < n && popc(S) < T; ++q) S |= 1ull << q;
+    return S;
+}
+
+uint32_t tile_positions(uint64_t gate_mask, uint64_t S) {
+    uint32_t pos = 0;
+    int m = 0;
+    for (uint64_t mk = gate_mask; mk; mk &= mk - 1, ++m) {
+        const int q = __builtin_ctzll(mk);
+        const int p = popc(S & low_mask(q));
+        pos |= (uint32_t)p << (4 * m);
+    }
+    return pos;
+}
+
+}  // namespace
+
+qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const ObsGroups& og,
+                          TrajProgram& out) {
+    out = TrajProgram();
+    const int n = P.n;
+    const int T = P.T;
+    out.records.assign(P.n_recorded, -1);
+    // ---- 1. draws + Alg. 2 first loop; build segments
+    std::vector<std::vector<Item>> segs(1);
+    struct Barrier { int event; uint64_t qmask; };
+    std::vector<Barrier> barriers;
+    for (const PlanOp& op : P.ops) {
+        if (op.kind == 0) {
+            if (!P.vars[op.var_base].identity)
+                segs.back().push_back(Item{op.mask, op.var_base, -1, op.nq});
+            continue;
+        }
+        const double u = draw(seed, (uint32_t)op.chan, kPurposeChannel, traj, 0);
+        double r = u;
+        int pick = -1;
+        for (int i = 0; i < op.n_kraus; ++i) {
+            if (r < op.pbar[i]) { pick = i; break; }
+            r -= op.pbar[i];
+        }
+        if (pick < 0 && op.mixture) pick = op.n_kraus - 1;  // s == 1
+        if (pick >= 0) {
+            ++out.n_deferred;
+            if (op.record >= 0) out.records[op.record] = pick;
+            const int v = op.var_base + pick;
+            if (!P.vars[v].identity) segs.back().push_back(Item{op.mask, v, -1, op.nq});
+            continue;
+        }
+        // conventional: barrier + device-chosen op opening the next segment
+        ++out.n_conventional;
+        EventDesc E;
+        E.chan = op.chan;
+        E.mat_off = 0;  // assigned below
+        E.record = op.record;
+        E.slot = 0;
+        E.r = r;
+        const int ev = (int)out.events.size();
+        out.events.push_back(E);
+        barriers.push_back(Barrier{ev, op.mask});
+        segs.emplace_back();
+        segs.back().push_back(Item{op.mask, -1, ev, op.nq});
+    }
+    // ---- 2.+3. fuse each segment, pack passes
+    const uint64_t lowS = low_mask(std::min(P.CL, n));
+    const uint64_t lowT = low_mask(T);
+    int32_t pool = 0;
+    std::vector<uint64_t> gate_masks;  // parallel to out.gates
+    auto alloc = [&](int d2) {
+        const int32_t off = pool;
+        pool += (d2 + 1) & ~1;  // keep 16-byte alignment
+        return off;
+    };
+    for (size_t si = 0; si < segs.size(); ++si) {
+        const std::vector<Item>& items = segs[si];
+        std::vector<FuseItem> fi(items.size());
+        for (size_t i = 0; i < items.size(); ++i) fi[i] = FuseItem{items[i].mask, items[i].var < 0};
+        std::vector<std::vector<int>> groups = fuse_items(fi, P.f);
+        std::vector<FusedGate> fg;
+        fg.reserve(groups.size());
+        for (auto& g : groups) {
+            FusedGate x;
+            x.mask = 0;
+            x.special_event = -1;
+            for (int it : g) x.mask |= items[it].mask;
+            if (g.size() == 1 && items[g[0]].var < 0) x.special_event = items[g[0]].event;
+            if (x.special_event < 0)
+                for (int it : g)
+                    if (items[it].var < 0) return QT_EINVAL;  // fixed item fused (cannot happen)
+            x.items = std::move(g);
+            fg.push_back(std::move(x));
+        }
+        // pass packing
+        std::vector<char> taken(fg.size(), 0);
+        size_t remaining = fg.size();
+        const bool last_seg = (si + 1 == segs.size());
+        std::vector<size_t> seg_pass_idx;
+        while (remaining > 0) {
+            uint64_t S = lowS;
+            uint64_t blocked = 0;
+            std::vector<int> chosen;
+            for (size_t i = 0; i < fg.size(); ++i) {
+                if (taken[i]) continue;
+                const uint64_t gm = fg[i].mask;
+                if (gm & blocked) { blocked |= gm; continue; }
+                if (popc(S | gm) <= T && (!P.one_gate || chosen.empty())) {
+                    S |= gm;
+                    chosen.push_back((int)i);
+                } else {
+                    blocked |= gm;
+                }
+            }
+            for (int i : chosen) taken[i] = 1;
+            remaining -= chosen.size();
+            PassDesc pd;
+            pd.tile_mask = S;  // filled below
+            pd.gate_begin = (int32_t)out.gates.size();
+            pd.gate_count = (int32_t)chosen.size();
+            pd.flags = kPassStore;
+            pd.event = -1;
+            pd.obs_begin = 0;
+            pd.obs_count = 0;
+            for (int i : chosen) {
+                FusedGate& g = fg[i];
+                GateDesc gd;
+                gd.k = popc(g.mask);
+                gd.pos = 0;  // after S is final
+                gd.pad = 0;
+                if (g.special_event >= 0) {
+                    const int d = 1 << gd.k;
+                    gd.mat_off = alloc(d * d);
+                    out.events[g.special_event].mat_off = gd.mat_off;
+                } else {
+                    const int d = 1 << gd.k;
+                    gd.mat_off = alloc(d * d);
+                    FusedDesc fd;
+                    fd.mat_off = gd.mat_off;
+                    fd.k = gd.k;
+                    fd.cons_begin = (int32_t)out.cons.size();
+                    fd.cons_count = (int32_t)g.items.size();
+                    for (int it : g.items) {
+                        ConsDesc c;
+                        c.var = items[it].var;
+                        uint32_t pos = 0;
+                        int m = 0;
+                        for (uint64_t mk = items[it].mask; mk; mk &= mk - 1, ++m) {
+                            const int q = __builtin_ctzll(mk);
+                            pos |= (uint32_t)popc(g.mask & low_mask(q)) << (4 * m);
+                        }
+                        c.pos = pos;
+                        out.cons.push_back(c);
+                    }
+                    out.fused.push_back(fd);
+                }
+                out.alg_flops += std::ldexp(1.0, n + gd.k + 3);
+                out.gates.push_back(gd);
+                gate_masks.push_back(g.mask);
+            }
+            seg_pass_idx.push_back(out.passes.size());
+            out.passes.push_back(pd);
+        }
+        // barrier epilogue: rho_Q of the next conventional channel
+        if (!last_seg) {
+            const Barrier& b = barriers[si];
+            if (seg_pass_idx.empty() || popc(out.passes[seg_pass_idx.back()].tile_mask | b.qmask) > T) {
+                PassDesc pd;
+                pd.tile_mask = lowS | b.qmask;
+                pd.gate_begin = (int32_t)out.gates.size();
+                pd.gate_count = 0;
+                pd.flags = 0;
+                pd.event = -1;
+                pd.obs_begin = pd.obs_count = 0;
+                seg_pass_idx.push_back(out.passes.size());
+                out.passes.push_back(pd);
+            }
+            PassDesc& lp = out.passes[seg_pass_idx.back()];
+            lp.tile_mask |= b.qmask;
+            lp.flags |= kPassRho;
+            lp.event = b.event;
+        }
+        // finalize tile masks, then tile-local gate positions
+        for (size_t pi : seg_pass_idx) {
+            PassDesc& pd = out.passes[pi];
+            pd.tile_mask = fill_tile(pd.tile_mask, T, n);
+            for (int g = 0; g < pd.gate_count; ++g) {
+                GateDesc& gd = out.gates[pd.gate_begin + g];
+                gd.pos = tile_positions(gate_masks[pd.gate_begin + g], pd.tile_mask);
+            }
+        }
+    }
+    // ---- 4. final epilogue: block sums over the low T qubits (+ observables of
+    // group 0), then read-only passes for the other observable groups
+    if (og.final_pass) {
+        const bool merge = !out.passes.empty() && out.passes.back().tile_mask == lowT &&
+                           !(out.passes.back().flags & kPassRho);
+        if (!merge) {
+            PassDesc pd;
+            pd.tile_mask = lowT;
+            pd.gate_begin = (int32_t)out.gates.size();
+            pd.gate_count = 0;
+            pd.flags = 0;
+            pd.event = -1;
+            pd.obs_begin = pd.obs_count = 0;
+            out.passes.push_back(pd);
+        }
+        PassDesc& fp = out.passes.back();
+        fp.flags |= kPassFinal;
+        if (!og.ranges.empty() && og.ranges[0].second > 0) {
+            fp.flags |= kPassObs;
+            fp.obs_begin = og.ranges[0].first;
+            fp.obs_count = og.ranges[0].second;
+        }
+        for (size_t k = 1; k < og.ranges.size(); ++k) {
+            PassDesc pd;
+            pd.tile_mask = og.masks[k];
+            pd.gate_begin = (int32_t)out.gates.size();
+            pd.gate_count = 0;
+            pd.flags = kPassObs;
+            pd.event = -1;
+            pd.obs_begin = og.ranges[k].first;
+            pd.obs_count = og.ranges[k].second;
+            out.passes.push_back(pd);
+        }
+    }
+    out.pool_size = pool;
+    // algorithmic bytes: 2^(n+4) per storing pass, 2^(n+3) per read-only pass
+    for (auto& pd : out.passes) out.alg_bytes += std::ldexp(1.0, n + ((pd.flags & kPassStore) ? 4 : 3));
+    return QT_OK;
+}
+
+}  // namespace qt
