@@ -24,16 +24,24 @@ struct PassDesc {
     int32_t event;        // EventDesc index (kPassRho) or -1
     int32_t obs_begin;    // into ObsDesc[] (kPassObs)
     int32_t obs_count;
+    uint8_t tq[12];       // global qubit of tile bit i (ascending), i < T
+    int32_t pad;
 };
 
-// A fused gate inside a pass.  pos = tile-local bit positions of the gate's
-// qubits, ascending, 4 bits each (matrix bit m <-> pos m).
+// A fused gate inside a pass and the register layout used to apply it:
+// register bit m of a thread's 2^R amplitudes <-> tile-local bit rpos[m]
+// (m < k: the gate's qubits ascending, so matrix bit m <-> register bit m;
+// m >= k: filler bits), thread-index bit i <-> tile-local bit tpos[i].
+// 4 bits per entry.
 struct GateDesc {
     int32_t mat_off;      // complex64 offset into the matrix pool (16-byte aligned)
     int32_t k;
-    uint32_t pos;
-    int32_t pad;
+    uint32_t rpos;
+    uint32_t tpos;
 };
+
+// Largest number of fused gates in one pass (descriptors staged in smem).
+constexpr int kMaxPassGates = 256;
 
 // A conventional channel occurrence (Alg. 2 lines 12-21).
 struct EventDesc {

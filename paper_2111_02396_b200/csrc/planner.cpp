@@ -262,15 +262,30 @@ uint64_t fill_tile(uint64_t S, int T, int n) {
     return S;
 }
 
-uint32_t tile_positions(uint64_t gate_mask, uint64_t S) {
-    uint32_t pos = 0;
+// Register layout of a fused gate inside a tile (see GateDesc): register bits
+// 0..k-1 = the gate's tile-local bits ascending, k..R-1 = the highest other
+// tile bits (so the lane bits stay low: bank-conflict-free re-layouts),
+// thread bits = the remaining tile bits ascending.
+void gate_layout(uint64_t gate_mask, uint64_t S, int T, int R, uint32_t& rpos, uint32_t& tpos) {
+    uint32_t regmask = 0;
+    rpos = 0;
     int m = 0;
     for (uint64_t mk = gate_mask; mk; mk &= mk - 1, ++m) {
         const int q = __builtin_ctzll(mk);
         const int p = popc(S & low_mask(q));
-        pos |= (uint32_t)p << (4 * m);
+        rpos |= (uint32_t)p << (4 * m);
+        regmask |= 1u << p;
     }
-    return pos;
+    for (int p = T - 1; p >= 0 && m < R; --p)
+        if (!((regmask >> p) & 1u)) {
+            rpos |= (uint32_t)p << (4 * m);
+            regmask |= 1u << p;
+            ++m;
+        }
+    tpos = 0;
+    int i = 0;
+    for (int p = 0; p < T; ++p)
+        if (!((regmask >> p) & 1u)) tpos |= (uint32_t)p << (4 * i++);
 }
 
 }  // namespace
@@ -362,7 +377,8 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
                 if (taken[i]) continue;
                 const uint64_t gm = fg[i].mask;
                 if (gm & blocked) { blocked |= gm; continue; }
-                if (popc(S | gm) <= T && (!P.one_gate || chosen.empty())) {
+                if (popc(S | gm) <= T && (!P.one_gate || chosen.empty()) &&
+                    (int)chosen.size() < kMaxPassGates) {
                     S |= gm;
                     chosen.push_back((int)i);
                 } else {
@@ -383,8 +399,7 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
                 FusedGate& g = fg[i];
                 GateDesc gd;
                 gd.k = popc(g.mask);
-                gd.pos = 0;  // after S is final
-                gd.pad = 0;
+                gd.rpos = gd.tpos = 0;  // after S is final
                 if (g.special_event >= 0) {
                     const int d = 1 << gd.k;
                     gd.mat_off = alloc(d * d);
@@ -443,7 +458,7 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
             pd.tile_mask = fill_tile(pd.tile_mask, T, n);
             for (int g = 0; g < pd.gate_count; ++g) {
                 GateDesc& gd = out.gates[pd.gate_begin + g];
-                gd.pos = tile_positions(gate_masks[pd.gate_begin + g], pd.tile_mask);
+                gate_layout(gate_masks[pd.gate_begin + g], pd.tile_mask, T, P.R, gd.rpos, gd.tpos);
             }
         }
     }
@@ -480,6 +495,12 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
             pd.obs_count = og.ranges[k].second;
             out.passes.push_back(pd);
         }
+    }
+    for (auto& pd : out.passes) {  // tile bit i -> global qubit
+        std::memset(pd.tq, 0, sizeof pd.tq);
+        int i = 0;
+        for (uint64_t mk = pd.tile_mask; mk; mk &= mk - 1) pd.tq[i++] = (uint8_t)__builtin_ctzll(mk);
+        pd.pad = 0;
     }
     out.pool_size = pool;
     // algorithmic bytes: 2^(n+4) per storing pass, 2^(n+3) per read-only pass

@@ -37,6 +37,11 @@ namespace detail {
 
 constexpr int kCL = 4;  // low qubits always inside a tile (128-byte runs)
 
+// CTAs per SM the (T = 12, R = 4) kernel is register-budgeted for.
+#ifndef QT_MINB
+#define QT_MINB 3
+#endif
+
 __device__ __forceinline__ uint32_t swz(uint32_t L) {
     // XOR-fold swizzle of the amplitude slot (linear over GF(2)):
     // bits 0..3 ^= bits 4..7 ^ bits 8..11.
@@ -68,6 +73,10 @@ __device__ __forceinline__ uint32_t pdep32(uint32_t x, uint32_t mask) {
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
@@ -127,12 +136,15 @@ __device__ __forceinline__ void apply_fused(float2* __restrict__ tile, const flo
             if ((r >> m) & 1) x ^= unit[m];
         return x;
     };
+    // unit[] / pbase are BYTE offsets: one 3-input XOR (LOP3) per shared access
+    char* const tb8 = reinterpret_cast<char*>(tile);
+    auto at = [&](uint32_t off) -> float2& { return *reinterpret_cast<float2*>(tb8 + off); };
     float2 a[NB * D];
 #pragma unroll
     for (int r = 0; r < D; ++r) {
         const uint32_t l = lo(r);
 #pragma unroll
-        for (int bb = 0; bb < NB; ++bb) a[bb * D + r] = tile[ahi[bb] ^ l];
+        for (int bb = 0; bb < NB; ++bb) a[bb * D + r] = at(ahi[bb] ^ l);
     }
     const float4* M4 = reinterpret_cast<const float4*>(M);
     // small gates: rows fully unrolled; K >= 5: row loop kept rolled (code size)
@@ -158,8 +170,17 @@ __device__ __forceinline__ void apply_fused(float2* __restrict__ tile, const flo
         }
         const uint32_t l = lo(r);
 #pragma unroll
-        for (int bb = 0; bb < NB; ++bb) tile[ahi[bb] ^ l] = acc[bb];
+        for (int bb = 0; bb < NB; ++bb) at(ahi[bb] ^ l) = acc[bb];
     }
+}
+
+// Global qubit mask -> tile-local bit mask (bits of the mask outside the tile dropped).
+template <int T>
+__device__ __forceinline__ uint32_t to_local(uint64_t m, const PassDesc& P) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int i = 0; i < T; ++i) r |= (uint32_t)((m >> P.tq[i]) & 1ull) << i;
+    return r;
 }
 
 template <int R>
@@ -181,15 +202,15 @@ template <int Q, int T, int NT>
 __device__ __forceinline__ void rho_partial(const float2* tile, uint32_t qlocal, double* out /*2*D*D*/, double* red) {
     constexpr int D = 1 << Q;
     const int tid = threadIdx.x;
-    const uint32_t rest_mask = ((1u << T) - 1u) & ~qlocal;
     uint32_t qoff[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) qoff[a] = pdep32((uint32_t)a, qlocal);
     double acc[2 * D * D];
 #pragma unroll
     for (int e = 0; e < 2 * D * D; ++e) acc[e] = 0.0;
-    for (uint32_t x = tid; x < (1u << (T - Q)); x += NT) {
-        const uint32_t bL = pdep32(x, rest_mask);
+    // every slot L with the channel bits clear is the base of one 2^Q group
+    for (uint32_t bL = tid; bL < (1u << T); bL += NT) {
+        if (bL & qlocal) continue;
         double vr[D], vi[D];
 #pragma unroll
         for (int a = 0; a < D; ++a) {
@@ -263,7 +284,7 @@ using namespace detail;
 // K1 tile pass
 // ---------------------------------------------------------------------------
 template <int T, int R>
-__global__ void __launch_bounds__(1 << (T - R))
+__global__ void __launch_bounds__(1 << (T - R), (R <= 4 && T == 12) ? QT_MINB : 1)
 tile_pass_kernel(const TileArgs A, const int step) {
     constexpr int NT = 1 << (T - R);
     constexpr int NA = 1 << R;
@@ -277,8 +298,9 @@ tile_pass_kernel(const TileArgs A, const int step) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float2* tile = reinterpret_cast<float2*>(smem_raw);
     float2* mbuf = tile + TILE;                                       // 2 x NA*NA
-    uint64_t* hoff = reinterpret_cast<uint64_t*>(mbuf + 2 * NA * NA);  // NH
-    double* red = reinterpret_cast<double*>(hoff + NH);               // 64
+    uint64_t* hoff = reinterpret_cast<uint64_t*>(mbuf + 2 * NA * NA);  // NH (padded to 16 B)
+    double* red = reinterpret_cast<double*>(hoff + ((NH + 1) & ~1));  // 64
+    GateDesc* gdesc = reinterpret_cast<GateDesc*>(red + 64);          // kMaxPassGates
     __shared__ int s_last;
 
     const int tid = threadIdx.x;
@@ -287,63 +309,55 @@ tile_pass_kernel(const TileArgs A, const int step) {
     const uint64_t base = pdep64((uint64_t)blockIdx.x, nmask & ~P.tile_mask);
     float2* st = A.state + ((uint64_t)slot << n);
 
-    // prefetch the first fused gate's matrix
-    if (P.gate_count > 0) {
-        const GateDesc G0 = A.gates[P.gate_begin];
-        const int chunks = (1 << (2 * G0.k)) >> 1;
-        for (int c = tid; c < chunks; c += NT) cp_async16(mbuf + 2 * c, A.pool + G0.mat_off + 2 * c);
-        cp_async_commit();
+    // stage the pass's gate descriptors and the first matrix (async)
+    const int ng = P.gate_count;
+    for (int c = tid; c < ng; c += NT) cp_async16(gdesc + c, A.gates + P.gate_begin + c);
+    cp_async_commit();
+    for (int h = tid; h < NH; h += NT) {
+        uint64_t o = 0;
+#pragma unroll
+        for (int i = CL; i < T; ++i) o |= (uint64_t)((h >> (i - CL)) & 1) << P.tq[i];
+        hoff[h] = o;
     }
-    for (int h = tid; h < NH; h += NT) hoff[h] = pdep64((uint64_t)h << CL, P.tile_mask);
     __syncthreads();
-
-    // HBM -> shared: 2^CL-amplitude contiguous runs, consecutive threads on consecutive amplitudes
+    // HBM -> shared, asynchronous 8-byte copies: 2^CL-amplitude contiguous runs,
+    // consecutive threads on consecutive amplitudes
 #pragma unroll
     for (int m = 0; m < NA; ++m) {
         const uint32_t L = (uint32_t)(tid + m * NT);
         const uint64_t g = base + hoff[L >> CL] + (L & ((1u << CL) - 1u));
-        tile[swz(L)] = st[g];
+        cp_async8(tile + swz(L), st + g);
     }
-
-    for (int gi = 0; gi < P.gate_count; ++gi) {
-        const GateDesc G = A.gates[P.gate_begin + gi];
+    cp_async_commit();
+    cp_async_wait_all();  // gate descriptors (the tile may still be in flight for other threads)
+    __syncthreads();
+    if (ng > 0) {
+        const int chunks = (1 << (2 * gdesc[0].k)) >> 1;
+        for (int c = tid; c < chunks; c += NT) cp_async16(mbuf + 2 * c, A.pool + gdesc[0].mat_off + 2 * c);
+        cp_async_commit();
+    }
+    for (int gi = 0; gi < ng; ++gi) {
+        const GateDesc G = gdesc[gi];
         cp_async_wait_all();
         __syncthreads();  // tile writes of the previous gate + this gate's matrix visible
-        if (gi + 1 < P.gate_count) {
-            const GateDesc Gn = A.gates[P.gate_begin + gi + 1];
+        if (gi + 1 < ng) {
+            const GateDesc Gn = gdesc[gi + 1];
             float2* dst = mbuf + ((gi + 1) & 1) * NA * NA;
             const int chunks = (1 << (2 * Gn.k)) >> 1;
             for (int c = tid; c < chunks; c += NT) cp_async16(dst + 2 * c, A.pool + Gn.mat_off + 2 * c);
             cp_async_commit();
         }
-        // register layout: bits 0..k-1 = gate qubits, k..R-1 = highest free tile bits
+        // register layout (host-computed): register bit m <-> tile bit rpos[m]
+        // (bits 0..k-1 = the gate qubits), thread bit i <-> tile bit tpos[i]
         uint32_t unit[R];
-        uint32_t regmask = 0;
 #pragma unroll
-        for (int m = 0; m < R; ++m) {
-            if (m < G.k) {
-                const uint32_t p = (G.pos >> (4 * m)) & 15u;
-                unit[m] = p;
-                regmask |= 1u << p;
-            }
-        }
-        {
-            int m = G.k;
-            for (int p = T - 1; p >= 0 && m < R; --p)
-                if (!((regmask >> p) & 1u)) {
+        for (int m = 0; m < R; ++m) unit[m] = swz(1u << ((G.rpos >> (4 * m)) & 15u)) << 3;
+        uint32_t tb = 0;
 #pragma unroll
-                    for (int mm = 0; mm < R; ++mm)
-                        if (mm == m) unit[mm] = (uint32_t)p;
-                    regmask |= 1u << p;
-                    ++m;
-                }
-        }
-#pragma unroll
-        for (int m = 0; m < R; ++m) unit[m] = swz(1u << unit[m]);
-        const uint32_t tb = pdep32((uint32_t)tid, ((1u << T) - 1u) & ~regmask);
-        const uint32_t pbase = swz(tb);
-        dispatch_fused<R>(G.k, tile, mbuf + (gi & 1) * NA * NA, pbase, unit);
+        for (int i = 0; i < T - R; ++i) tb |= (((uint32_t)tid >> i) & 1u) << ((G.tpos >> (4 * i)) & 15u);
+        dispatch_fused<R>(G.k, tile, mbuf + (gi & 1) * NA * NA, swz(tb) << 3, unit);
     }
+    cp_async_wait_all();  // a pass without gates still has its tile in flight
     __syncthreads();
 
     // ---- epilogues (read-only on the tile) ----
@@ -353,17 +367,7 @@ tile_pass_kernel(const TileArgs A, const int step) {
         const EventDesc E = A.events[P.event];
         const ChanDesc C = A.chans[E.chan];
         const uint64_t qmask = C.qmask;
-        uint32_t ql = 0;  // channel qubits as tile-local bit positions
-        {
-            uint64_t tm = P.tile_mask;
-            int pos = 0;
-            while (tm) {
-                const uint64_t low = tm & (~tm + 1);
-                if (qmask & low) ql |= 1u << pos;
-                ++pos;
-                tm ^= low;
-            }
-        }
+        const uint32_t ql = to_local<T>(qmask, P);  // channel qubits as tile-local bits
         double* out = A.rho_part + tile_row * A.rho_stride;
         if constexpr (T >= 2) {
             if (C.nq == 1) rho_partial<1, T, NT>(tile, ql, out, red);
@@ -406,20 +410,20 @@ tile_pass_kernel(const TileArgs A, const int step) {
         for (int o = 0; o < P.obs_count; ++o) {
             const ObsDesc O = A.obs[P.obs_begin + o];
             const uint64_t xo = O.xmask & ~P.tile_mask;
-            uint32_t xl = 0, zl = 0;
-            {
-                uint64_t tm = P.tile_mask;
-                int pos = 0;
-                while (tm) {
-                    const uint64_t low = tm & (~tm + 1);
-                    if (O.xmask & low) xl |= 1u << pos;
-                    if (O.zmask & low) zl |= 1u << pos;
-                    ++pos;
-                    tm ^= low;
-                }
-            }
+            const uint32_t xl = to_local<T>(O.xmask, P), zl = to_local<T>(O.zmask, P);
             const int zs = __popcll(base & O.zmask) & 1;
             double s = 0.0;
+            if (O.xmask == 0) {  // Z-type string: sum of +-|psi_L|^2 (fp32 per thread, fp64 across)
+                float sf = 0.f;
+#pragma unroll
+                for (int m = 0; m < NA; ++m) {
+                    const uint32_t L = (uint32_t)(tid + m * NT);
+                    const float2 v = tile[swz(L)];
+                    const float p = fmaf(v.x, v.x, v.y * v.y);
+                    sf += (__popc(L & zl) & 1) ? -p : p;
+                }
+                s = zs ? -(double)sf : (double)sf;
+            } else
             for (int m = 0; m < NA; ++m) {
                 const uint32_t L = (uint32_t)(tid + m * NT);
                 const float2 v = tile[swz(L)];
@@ -463,8 +467,8 @@ inline size_t tile_pass_smem_bytes_impl(int T, int R) {
     const int CL = T < kCL ? T : kCL;
     const size_t tile = sizeof(float2) << T;
     const size_t mb = 2 * sizeof(float2) * ((size_t)1 << (2 * R));
-    const size_t hoff = sizeof(uint64_t) * ((size_t)1 << (T - CL));
-    return tile + mb + hoff + 64 * sizeof(double);
+    const size_t hoff = sizeof(uint64_t) * ((((size_t)1 << (T - CL)) + 1) & ~(size_t)1);
+    return tile + mb + hoff + 64 * sizeof(double) + sizeof(GateDesc) * kMaxPassGates;
 }
 
 template <int T, int R>
