@@ -267,6 +267,15 @@ def bench_gpu(args):
         roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": frac_hbm,
                 "traffic": None, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
                 "alu": {"achieved_tflops": achieved_tf, "peak_tflops": fp32_peak_tf, "frac": frac_alu}}
+    # traffic: DRAM bytes per launch from the committed ncu --set full capture,
+    # scaled to this run's average launch (ratio dram/algorithmic of that capture)
+    tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    if os.path.exists(tpath):
+        tr = json.load(open(tpath))
+        roof["traffic"] = tr["ratio"] * alg_bytes / max(pass_launches, 1)
+        roof["traffic_unit"] = "bytes/launch"
+        roof["traffic_source"] = tr["source"]
+    roof["alg_bytes_per_launch"] = alg_bytes / max(pass_launches, 1)
     roof["kernel"] = "tile_pass_kernel<12,4>"
     roof["launches_timed"] = int(pass_launches)
     roof["avg_launch_ms"] = pass_ms / max(pass_launches, 1)
