@@ -160,6 +160,30 @@ def circuit_bytes(circ):
     return b + 2 * 8 * circ.n_qubits
 
 
+def gate_pass_sweep(ctx, n, dev, hbm_peak, reps=10):
+    """Isolated K1 passes of Haar k-qubit gates, k = 1..6, placements all-low,
+    all-high and one random mixed; GB/s = 2^(n+4) / t."""
+    import torch
+    rng = np.random.default_rng(workloads.circuit_seed(4))
+    state = torch.zeros(1 << n, dtype=torch.complex64, device=dev)
+    state[0] = 1.0
+    rows = []
+    for k in range(1, 7):
+        places = {"low": list(range(k)), "high": list(range(n - k, n)),
+                  "mixed": sorted(int(x) for x in rng.choice(n, size=k, replace=False))}
+        for name, qs in places.items():
+            U = workloads.haar_unitary(rng, 2 ** k)
+            ms = ctx.apply_gate(state, qs, U, repeats=reps + 1)  # first application = warm-up
+            gbs = 2.0 ** (n + 4) / (ms / 1e3) / 1e9
+            rows.append({"k": k, "placement": name, "qubits": qs, "ms": ms, "gbs": gbs, "frac": gbs / hbm_peak})
+    torch.cuda.synchronize()
+    best = max(r["gbs"] for r in rows)
+    med = float(np.median([r["gbs"] for r in rows]))
+    return {"n": n, "bytes_per_pass": 2 ** (n + 4), "peak_gbs": hbm_peak, "best_gbs": best, "median_gbs": med,
+            "best_frac": best / hbm_peak, "median_frac": med / hbm_peak,
+            "k4_median_frac": float(np.median([r["frac"] for r in rows if r["k"] <= 4])), "rows": rows}
+
+
 def bench_gpu(args):
     import torch
     import torch.distributed as dist
@@ -281,6 +305,14 @@ def bench_gpu(args):
     roof["avg_launch_ms"] = pass_ms / max(pass_launches, 1)
     roof["share_of_step"] = pass_ms / tot_ms if tot_ms else None
 
+    # ---- gate-pass HBM GB/s vs peak (second half of the metric; SURVEY 8(d) C4 sweep
+    # at n = sweep_n): one fused k-qubit Haar gate per HBM sweep, 2^(n+4) bytes per pass
+    sweep = None
+    if rank == 0 and args.sweep_n > 0:
+        del state
+        torch.cuda.empty_cache()
+        sweep = gate_pass_sweep(ctx, args.sweep_n, dev, hbm_peak)
+
     # ---- CPU oracle baseline (rank 0, N = 1 only, bounded sample)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -303,6 +335,7 @@ def bench_gpu(args):
             "gpu_launches": int(sum(s["launches"] for s in stats)),
             "roofline": roof,
             "cpu_baseline": cpu,
+            "gate_pass_sweep": sweep,
             "clocks": clocks,
             "per_step_stats": {"passes_per_traj": st["passes"] / max(st["trajectories"], 1),
                                "fused_gates_per_traj": st["fused_gates"] / max(st["trajectories"], 1),
@@ -327,6 +360,7 @@ def main():
     ap.add_argument("--fuse", type=int, default=4)
     ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep-n", type=int, default=30, help="qubits of the gate-pass bandwidth sweep (0 = skip)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

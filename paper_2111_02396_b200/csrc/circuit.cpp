@@ -286,6 +286,18 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
     }
     P.f = std::min(f, P.R);
     P.one_gate = o.one_gate_per_pass != 0;
+    // tensor cores: every fused gate padded to 4 qubits (f <= 4), T = 12, 128-thread CTAs
+    // whose CUDA-core gates use R = 5
+    const bool tc_ok = (P.T == 12 && f <= 4 && max_arity <= 4);
+    if (o.tensor_cores > 0 && !tc_ok) {
+        delete hp;
+        return fail(QT_EINVAL, "tensor_cores needs n >= 12, max_fused <= 4 and gates of <= 4 qubits");
+    }
+    P.tc = o.tensor_cores >= 0 && tc_ok;
+    if (P.tc) {
+        P.R = 5;  // 128-thread CTAs (4 per SM), two 16-amplitude subvectors per thread
+        P.f = f;
+    }
     // canonical order: moment ascending, then call order (stable)
     std::vector<const HostOp*> order;
     for (auto& op : C.ops) order.push_back(&op);

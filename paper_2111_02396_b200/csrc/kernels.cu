@@ -25,21 +25,23 @@
 
 #include "kernels.hpp"
 #include "philox.hpp"
-#include "tile_pass.cuh"
+#include "tile_pass_kernel.cuh"
 
 namespace qt {
 
-// Tile-pass instantiations live in tile_pass_r{4,5,6}.cu (parallel compile).
+// Tile-pass instantiations live in tile_pass_{r4,r5,r6,tc}.cu (parallel compile).
 cudaError_t launch_tile_pass_r4(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s);
 cudaError_t launch_tile_pass_r5(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s);
 cudaError_t launch_tile_pass_r6(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s);
+cudaError_t launch_tile_pass_tc(const TileArgs& a, int R, int step, uint32_t ntiles, int nslots, cudaStream_t s);
 
-size_t tile_pass_smem_bytes(int T, int R) { return tile_pass_smem_bytes_impl(T, R); }
+size_t tile_pass_smem_bytes(int T, int R, bool tcm) { return tile_pass_smem_bytes_impl(T, R, tcm); }
 
-cudaError_t launch_tile_pass(const TileArgs& a, int R, int step, uint32_t ntiles, int nslots,
+cudaError_t launch_tile_pass(const TileArgs& a, int R, bool tcm, int step, uint32_t ntiles, int nslots,
                              cudaStream_t s) {
     // Instantiated (T, R): (12, 4), (12, 5), (12, 6) and (T, min(T, 4)) for
-    // T = 1..11 (the whole state of n < 12 qubits in one CTA).
+    // T = 1..11 (the whole state of n < 12 qubits in one CTA); tensor cores: (12, 5).
+    if (tcm) return a.T == 12 ? launch_tile_pass_tc(a, R, step, ntiles, nslots, s) : cudaErrorInvalidValue;
     if (a.T == 12 && R == 6) return launch_tile_pass_r6(a, step, ntiles, nslots, s);
     if (a.T == 12 && R == 5) return launch_tile_pass_r5(a, step, ntiles, nslots, s);
     if (R == (a.T < 4 ? a.T : 4)) return launch_tile_pass_r4(a, step, ntiles, nslots, s);
@@ -55,7 +57,8 @@ materialize_kernel(const FusedDesc* __restrict__ fused, const ConsDesc* __restri
                    const VarDesc* __restrict__ vars, const double2* __restrict__ var_data,
                    float2* __restrict__ pool) {
     const FusedDesc F = fused[blockIdx.x];
-    const int D = 1 << F.k;
+    const bool tcm = (F.k & kGateTC) != 0;
+    const int D = 1 << (F.k & 0xff);
     const int c = threadIdx.x;
     if (c >= D) return;
     double2 v[64];
@@ -94,7 +97,26 @@ materialize_kernel(const FusedDesc* __restrict__ fused, const ConsDesc* __restri
             }
         }
     }
-    for (int rr = 0; rr < D; ++rr) pool[F.mat_off + rr * D + c] = make_float2((float)v[rr].x, (float)v[rr].y);
+    if (!tcm) {
+        for (int rr = 0; rr < D; ++rr) pool[F.mat_off + rr * D + c] = make_float2((float)v[rr].x, (float)v[rr].y);
+        return;
+    }
+    // tensor-core operand W (tc_common.cuh): W[2c + a][2j + b] = real 2x2 block of
+    // U[j][c], stored K-major swizzled as hi then lo tf32 parts.  Column c of U = v.
+    uint32_t* W = reinterpret_cast<uint32_t*>(pool + F.mat_off);
+    for (int j = 0; j < D; ++j) {
+        const double ur = v[j].x, ui = v[j].y;
+        const double blk[2][2] = {{ur, ui}, {-ui, ur}};
+        for (int a = 0; a < 2; ++a)
+            for (int b = 0; b < 2; ++b) {
+                const float w = (float)blk[a][b];
+                const uint32_t h = tc::tf32_rna(w);
+                const uint32_t l = tc::tf32_rna(w - __uint_as_float(h));
+                const uint32_t off = tc::w_offset_bytes(2 * j + b, 2 * c + a) >> 2;
+                W[off] = h;
+                W[(tc::kWBytes >> 2) + off] = l;
+            }
+    }
 }
 
 cudaError_t launch_materialize(const FusedDesc* fused, int n_fused, const ConsDesc* cons,

@@ -36,8 +36,8 @@ struct TileArgs {
 constexpr int kMaxR = 6;
 constexpr int kMaxT = 12;
 
-size_t tile_pass_smem_bytes(int T, int R);
-cudaError_t launch_tile_pass(const TileArgs& a, int R, int step, uint32_t ntiles, int nslots,
+size_t tile_pass_smem_bytes(int T, int R, bool tcm);
+cudaError_t launch_tile_pass(const TileArgs& a, int R, bool tcm, int step, uint32_t ntiles, int nslots,
                              cudaStream_t s);
 
 cudaError_t launch_materialize(const FusedDesc* fused, int n_fused, const ConsDesc* cons,

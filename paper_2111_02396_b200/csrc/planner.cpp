@@ -405,11 +405,16 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
                     gd.mat_off = alloc(d * d);
                     out.events[g.special_event].mat_off = gd.mat_off;
                 } else {
-                    const int d = 1 << gd.k;
-                    gd.mat_off = alloc(d * d);
+                    // tensor cores: pad the fused gate to 4 qubits with the lowest
+                    // qubits it does not touch (always inside the tile)
+                    uint64_t pm = g.mask;
+                    if (P.tc)
+                        for (int q = 0; q < n && popc(pm) < 4; ++q) pm |= 1ull << q;
+                    const int d = 1 << popc(pm);
+                    gd.mat_off = alloc(P.tc ? kGateTCPoolEntries : d * d);
                     FusedDesc fd;
                     fd.mat_off = gd.mat_off;
-                    fd.k = gd.k;
+                    fd.k = popc(pm) | (P.tc ? kGateTC : 0);
                     fd.cons_begin = (int32_t)out.cons.size();
                     fd.cons_count = (int32_t)g.items.size();
                     for (int it : g.items) {
@@ -419,14 +424,19 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
                         int m = 0;
                         for (uint64_t mk = items[it].mask; mk; mk &= mk - 1, ++m) {
                             const int q = __builtin_ctzll(mk);
-                            pos |= (uint32_t)popc(g.mask & low_mask(q)) << (4 * m);
+                            pos |= (uint32_t)popc(pm & low_mask(q)) << (4 * m);
                         }
                         c.pos = pos;
                         out.cons.push_back(c);
                     }
                     out.fused.push_back(fd);
+                    if (P.tc) {
+                        gd.k |= kGateTC;
+                        g.mask = pm;  // layout over the padded qubit set
+                    }
                 }
-                out.alg_flops += std::ldexp(1.0, n + gd.k + 3);
+                out.alg_flops += std::ldexp(1.0, n + (gd.k & 0xff) + 3);
+                if (P.tc && (gd.k & kGateTC)) gd.k = 4 | kGateTC;
                 out.gates.push_back(gd);
                 gate_masks.push_back(g.mask);
             }

@@ -30,6 +30,7 @@
 
 #include "kernels.hpp"
 #include "philox.hpp"
+#include "tc_common.cuh"
 
 namespace qt {
 
@@ -280,210 +281,5 @@ static __device__ __noinline__ void choose_conventional(const EventDesc& E, cons
 }  // namespace detail
 using namespace detail;
 
-// ---------------------------------------------------------------------------
-// K1 tile pass
-// ---------------------------------------------------------------------------
-template <int T, int R>
-__global__ void __launch_bounds__(1 << (T - R), (R <= 4 && T == 12) ? QT_MINB : 1)
-tile_pass_kernel(const TileArgs A, const int step) {
-    constexpr int NT = 1 << (T - R);
-    constexpr int NA = 1 << R;
-    constexpr int TILE = 1 << T;
-    constexpr int CL = T < kCL ? T : kCL;
-    constexpr int NH = TILE >> CL;
-    const int slot = blockIdx.y;
-    if (step >= A.pass_count[slot]) return;
-    const PassDesc P = A.passes[A.pass_start[slot] + step];
-
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    float2* tile = reinterpret_cast<float2*>(smem_raw);
-    float2* mbuf = tile + TILE;                                       // 2 x NA*NA
-    uint64_t* hoff = reinterpret_cast<uint64_t*>(mbuf + 2 * NA * NA);  // NH (padded to 16 B)
-    double* red = reinterpret_cast<double*>(hoff + ((NH + 1) & ~1));  // 64
-    GateDesc* gdesc = reinterpret_cast<GateDesc*>(red + 64);          // kMaxPassGates
-    __shared__ int s_last;
-
-    const int tid = threadIdx.x;
-    const int n = A.n;
-    const uint64_t nmask = (n >= 64) ? ~0ull : ((1ull << n) - 1ull);
-    const uint64_t base = pdep64((uint64_t)blockIdx.x, nmask & ~P.tile_mask);
-    float2* st = A.state + ((uint64_t)slot << n);
-
-    // stage the pass's gate descriptors and the first matrix (async)
-    const int ng = P.gate_count;
-    for (int c = tid; c < ng; c += NT) cp_async16(gdesc + c, A.gates + P.gate_begin + c);
-    cp_async_commit();
-    for (int h = tid; h < NH; h += NT) {
-        uint64_t o = 0;
-#pragma unroll
-        for (int i = CL; i < T; ++i) o |= (uint64_t)((h >> (i - CL)) & 1) << P.tq[i];
-        hoff[h] = o;
-    }
-    __syncthreads();
-    // HBM -> shared, asynchronous 8-byte copies: 2^CL-amplitude contiguous runs,
-    // consecutive threads on consecutive amplitudes
-#pragma unroll
-    for (int m = 0; m < NA; ++m) {
-        const uint32_t L = (uint32_t)(tid + m * NT);
-        const uint64_t g = base + hoff[L >> CL] + (L & ((1u << CL) - 1u));
-        cp_async8(tile + swz(L), st + g);
-    }
-    cp_async_commit();
-    cp_async_wait_all();  // gate descriptors (the tile may still be in flight for other threads)
-    __syncthreads();
-    if (ng > 0) {
-        const int chunks = (1 << (2 * gdesc[0].k)) >> 1;
-        for (int c = tid; c < chunks; c += NT) cp_async16(mbuf + 2 * c, A.pool + gdesc[0].mat_off + 2 * c);
-        cp_async_commit();
-    }
-    for (int gi = 0; gi < ng; ++gi) {
-        const GateDesc G = gdesc[gi];
-        cp_async_wait_all();
-        __syncthreads();  // tile writes of the previous gate + this gate's matrix visible
-        if (gi + 1 < ng) {
-            const GateDesc Gn = gdesc[gi + 1];
-            float2* dst = mbuf + ((gi + 1) & 1) * NA * NA;
-            const int chunks = (1 << (2 * Gn.k)) >> 1;
-            for (int c = tid; c < chunks; c += NT) cp_async16(dst + 2 * c, A.pool + Gn.mat_off + 2 * c);
-            cp_async_commit();
-        }
-        // register layout (host-computed): register bit m <-> tile bit rpos[m]
-        // (bits 0..k-1 = the gate qubits), thread bit i <-> tile bit tpos[i]
-        uint32_t unit[R];
-#pragma unroll
-        for (int m = 0; m < R; ++m) unit[m] = swz(1u << ((G.rpos >> (4 * m)) & 15u)) << 3;
-        uint32_t tb = 0;
-#pragma unroll
-        for (int i = 0; i < T - R; ++i) tb |= (((uint32_t)tid >> i) & 1u) << ((G.tpos >> (4 * i)) & 15u);
-        dispatch_fused<R>(G.k, tile, mbuf + (gi & 1) * NA * NA, swz(tb) << 3, unit);
-    }
-    cp_async_wait_all();  // a pass without gates still has its tile in flight
-    __syncthreads();
-
-    // ---- epilogues (read-only on the tile) ----
-    const uint32_t ntiles = gridDim.x;
-    const uint64_t tile_row = (uint64_t)slot * ntiles + blockIdx.x;
-    if (P.flags & kPassRho) {
-        const EventDesc E = A.events[P.event];
-        const ChanDesc C = A.chans[E.chan];
-        const uint64_t qmask = C.qmask;
-        const uint32_t ql = to_local<T>(qmask, P);  // channel qubits as tile-local bits
-        double* out = A.rho_part + tile_row * A.rho_stride;
-        if constexpr (T >= 2) {
-            if (C.nq == 1) rho_partial<1, T, NT>(tile, ql, out, red);
-            else rho_partial<2, T, NT>(tile, ql, out, red);
-        } else {
-            rho_partial<1, T, NT>(tile, ql, out, red);
-        }
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) s_last = (atomicAdd(&A.counters[slot], 1) == (int)ntiles - 1);
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            const int ne = 2 * C.d * C.d;
-            double* fin = red;  // ne <= 32 doubles
-            for (int e = tid; e < ne; e += NT) {
-                double s = 0.0;
-                for (uint32_t t = 0; t < ntiles; ++t)
-                    s += __ldcg(A.rho_part + ((uint64_t)slot * ntiles + t) * A.rho_stride + e);
-                fin[e] = s;
-            }
-            __syncthreads();
-            if (tid == 0) {
-                choose_conventional(E, C, A.chan_data, fin, A.pool, A.records, A.status + slot);
-                A.counters[slot] = 0;
-            }
-        }
-    }
-    if (P.flags & kPassFinal) {
-        double s = 0.0;
-#pragma unroll 4
-        for (int m = 0; m < NA; ++m) {
-            const float2 v = tile[swz((uint32_t)(tid + m * NT))];
-            s += (double)v.x * v.x + (double)v.y * v.y;
-        }
-        s = block_sum<NT>(s, red);
-        if (tid == 0) A.blocksum[tile_row] = s;
-    }
-    if (P.flags & kPassObs) {
-        for (int o = 0; o < P.obs_count; ++o) {
-            const ObsDesc O = A.obs[P.obs_begin + o];
-            const uint64_t xo = O.xmask & ~P.tile_mask;
-            const uint32_t xl = to_local<T>(O.xmask, P), zl = to_local<T>(O.zmask, P);
-            const int zs = __popcll(base & O.zmask) & 1;
-            double s = 0.0;
-            if (O.xmask == 0) {  // Z-type string: sum of +-|psi_L|^2 (fp32 per thread, fp64 across)
-                float sf = 0.f;
-#pragma unroll
-                for (int m = 0; m < NA; ++m) {
-                    const uint32_t L = (uint32_t)(tid + m * NT);
-                    const float2 v = tile[swz(L)];
-                    const float p = fmaf(v.x, v.x, v.y * v.y);
-                    sf += (__popc(L & zl) & 1) ? -p : p;
-                }
-                s = zs ? -(double)sf : (double)sf;
-            } else
-            for (int m = 0; m < NA; ++m) {
-                const uint32_t L = (uint32_t)(tid + m * NT);
-                const float2 v = tile[swz(L)];
-                float2 w;
-                if (xo == 0) {
-                    w = tile[swz(L ^ xl)];
-                } else {  // partner amplitude in another tile (read-only pass only)
-                    const uint64_t g = base + hoff[L >> CL] + (L & ((1u << CL) - 1u));
-                    w = st[g ^ O.xmask];
-                }
-                // c = conj(w) * v
-                const double cr = (double)w.x * v.x + (double)w.y * v.y;
-                const double ci = (double)w.x * v.y - (double)w.y * v.x;
-                double t;
-                switch (O.ny & 3) {
-                    case 0: t = cr; break;
-                    case 1: t = -ci; break;
-                    case 2: t = -cr; break;
-                    default: t = ci; break;
-                }
-                const int par = (__popc(L & zl) + zs) & 1;
-                s += par ? -t : t;
-            }
-            s = block_sum<NT>(s, red);
-            if (tid == 0) A.obs_part[tile_row * A.n_obs + O.slot] = s;
-        }
-    }
-
-    // ---- shared -> HBM ----
-    if (P.flags & kPassStore) {
-#pragma unroll
-        for (int m = 0; m < NA; ++m) {
-            const uint32_t L = (uint32_t)(tid + m * NT);
-            const uint64_t g = base + hoff[L >> CL] + (L & ((1u << CL) - 1u));
-            st[g] = tile[swz(L)];
-        }
-    }
-}
-
-inline size_t tile_pass_smem_bytes_impl(int T, int R) {
-    const int CL = T < kCL ? T : kCL;
-    const size_t tile = sizeof(float2) << T;
-    const size_t mb = 2 * sizeof(float2) * ((size_t)1 << (2 * R));
-    const size_t hoff = sizeof(uint64_t) * ((((size_t)1 << (T - CL)) + 1) & ~(size_t)1);
-    return tile + mb + hoff + 64 * sizeof(double) + sizeof(GateDesc) * kMaxPassGates;
-}
-
-template <int T, int R>
-cudaError_t launch_tr(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s) {
-    const size_t smem = tile_pass_smem_bytes_impl(T, R);
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(tile_pass_kernel<T, R>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    dim3 grid(ntiles, nslots);
-    tile_pass_kernel<T, R><<<grid, 1 << (T - R), smem, s>>>(a, step);
-    return cudaGetLastError();
-}
-
 }  // namespace qt
+

@@ -43,7 +43,8 @@ class Stats(ctypes.Structure):
 
 class FuseOpts(ctypes.Structure):
     _fields_ = [("max_fused", ctypes.c_int), ("tile_bits", ctypes.c_int),
-                ("low_bits", ctypes.c_int), ("one_gate_per_pass", ctypes.c_int)]
+                ("low_bits", ctypes.c_int), ("one_gate_per_pass", ctypes.c_int),
+                ("tensor_cores", ctypes.c_int)]
 
 
 class RunOpts(ctypes.Structure):
@@ -180,9 +181,9 @@ class Plan:
     """Owning handle of a qt_plan (the paper's fuser, Sec. III.B)."""
 
     def __init__(self, circuit: Circuit, max_fused: int = 4, tile_bits: int = 0, low_bits: int = 0,
-                 one_gate_per_pass: bool = False):
+                 one_gate_per_pass: bool = False, tensor_cores: int = 0):
         h = ctypes.c_void_p()
-        o = FuseOpts(max_fused, tile_bits, low_bits, int(one_gate_per_pass))
+        o = FuseOpts(max_fused, tile_bits, low_bits, int(one_gate_per_pass), int(tensor_cores))
         _check(lib().qt_fuse_ex(circuit.h, ctypes.byref(o), ctypes.byref(h)))
         self.h = h
         self.n = circuit.n

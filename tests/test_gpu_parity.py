@@ -92,11 +92,12 @@ def test_all_placements_n10_k2(ctx):
 # ---------------------------------------------------------------------------
 # Trajectories (Alg. 2) vs the oracle, element by element
 # ---------------------------------------------------------------------------
-def run_both(ctx, c, seed, T, shots=1, f=4, batch=0, one_gate=False, traj_begin=0, stride=1):
+def run_both(ctx, c, seed, T, shots=1, f=4, batch=0, one_gate=False, traj_begin=0, stride=1, tensor_cores=0):
     ref = oracle.run_trajectories(c, seed=seed, traj_begin=traj_begin, stride=stride, traj_count=T,
                                   shots=shots, want_states=True)
     assert ref["rc"] == 0
-    plan = qtraj.Plan(qtraj.Circuit.from_description(c), max_fused=f, one_gate_per_pass=one_gate)
+    plan = qtraj.Plan(qtraj.Circuit.from_description(c), max_fused=f, one_gate_per_pass=one_gate,
+                      tensor_cores=tensor_cores)
     if batch == 0:
         batch = T  # one batch: the state buffer then holds every final state
     state = torch.zeros(batch << c.n_qubits, dtype=torch.complex64, device="cuda")
@@ -146,6 +147,16 @@ def test_random_noisy_trajectories(ctx, noise, n):
     compare(ref, out, state)
     if noise in ("decay", "both", "ad", "pd"):
         assert out["stats"]["reductions"] > 0
+
+
+@pytest.mark.parametrize("tensor_cores", [-1, 1])
+@pytest.mark.parametrize("n", [12, 14])
+def test_tensor_core_and_cuda_core_paths(ctx, n, tensor_cores):
+    """K1 on tcgen05 (3xTF32, gates padded to 4 qubits) and on FP32 CUDA cores."""
+    c = workloads.random_circuit(n, depth=10, seed=300 + n, max_arity=2, noise="both", p=0.03,
+                                 t1_ns=700.0, tphi_ns=1200.0, readout=True)
+    ref, out, state = run_both(ctx, c, seed=17, T=10, shots=2, tensor_cores=tensor_cores)
+    compare(ref, out, state)
 
 
 @pytest.mark.parametrize("f", [2, 3, 4, 5, 6])
