@@ -143,7 +143,10 @@ void qt_plan_destroy(qt_plan p);
  * out_kraus: host, traj_count * qt_circuit_num_recorded int32 (chosen Kraus
  *   index of each recorded channel, in canonical order), or NULL.
  * out_obs  : host, traj_count * n_obs doubles: <psi|P|psi>/<psi|psi>, or NULL.
- * mode: 0 = delayed inner product (Alg. 2).  Others are reserved. */
+ * mode: 0 = delayed inner product (Alg. 2).  1 = the conventional
+ *   trajectory algorithm the paper compares against: no lower bounds,
+ *   every channel is a barrier whose p_i are computed on the device (same
+ *   draws, same literal subtract loop with pbar_i = 0); channels of <= 2 qubits. */
 typedef struct {
     uint64_t seed;
     uint64_t traj_begin;

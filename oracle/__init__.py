@@ -63,7 +63,7 @@ def lib():
         L.orc_run_trajectories.argtypes = (
             [ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, vp,
              ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64,
-             ctypes.c_int, ctypes.c_int] + [vp] * 9)
+             ctypes.c_int, ctypes.c_int, ctypes.c_int] + [vp] * 9)
         L.orc_run_trajectories.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -134,9 +134,11 @@ class TrajectoryResult(dict):
 
 def run_trajectories(circuit, seed: int, traj_begin: int = 0, traj_count: int = 1,
                      stride: int = 1, shots: int = 1, threads: int = None,
-                     want_states: bool = False) -> TrajectoryResult:
+                     want_states: bool = False, mode: int = 0) -> TrajectoryResult:
     """Alg. 2 trajectories t = traj_begin + stride*j, j < traj_count.
 
+    mode 0 = delayed inner products (Alg. 2); mode 1 = the conventional
+    trajectory algorithm (every channel computes its p_i).
     `circuit` is a workloads.Circuit.  Returns numpy arrays keyed by name."""
     from workloads import flatten  # input serialization only
     f = flatten(circuit)
@@ -163,7 +165,7 @@ def run_trajectories(circuit, seed: int, traj_begin: int = 0, traj_count: int = 
         n, n_ops, _ptr(f["kind"]), _ptr(f["nq"]), _ptr(qubits), _ptr(f["n_kraus"]),
         _ptr(f["mat_off"]), _ptr(f["mats"]), _ptr(p00), _ptr(p11), n_obs,
         ctypes.addressof(obs_buf) if obs_buf is not None else None,
-        seed, traj_begin, stride, T, shots, threads,
+        seed, traj_begin, stride, T, shots, threads, mode,
         _ptr(states), _ptr(out["kraus"]), _ptr(out["branch"]), _ptr(out["kraus_margin"]),
         _ptr(out["bits"]), _ptr(out["bits_raw"]), _ptr(out["sample_margin"]),
         _ptr(out["obs"]), _ptr(out["status"]))

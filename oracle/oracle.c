@@ -255,6 +255,7 @@ typedef struct {
     const double* p11;
     int n_obs;
     const char* obs;     /* n_obs * n chars of 'I','X','Y','Z'; char q = qubit q */
+    int mode;            /* 0 = Alg. 2 (delayed), 1 = conventional */
 } orc_circuit;
 
 typedef struct {
@@ -271,8 +272,12 @@ typedef struct {
 static double min_d(double a, double b) { return a < b ? a : b; }
 
 /* Alg. 2 for one channel; returns status. psi is normalized on entry. */
+/* mode 0: Alg. 2 (delayed inner products).  mode 1: the conventional
+ * trajectory algorithm of P:181 -- no lower bounds (pbar_i = 0), so every
+ * channel computes its p_i = ||K_i psi||^2 and samples with the same literal
+ * subtract loop (Alg. 2's second loop with pbar = 0). */
 static int sample_channel(cplx* psi, int n, int nq, const int* qubits, int nk,
-                          const cplx* Ks, double u, int* chosen, int* branch,
+                          const cplx* Ks, double u, int mode, int* chosen, int* branch,
                           double* margin) {
     int d = 1 << nq;
     double pbar[64];
@@ -283,6 +288,10 @@ static int sample_channel(cplx* psi, int n, int nq, const int* qubits, int nk,
     }
     (void)s;
     int mixture = is_unitary_mixture(d, nk, Ks);
+    if (mode == 1) {
+        for (int i = 0; i < nk; ++i) pbar[i] = 0.0;
+        mixture = 0;
+    }
     double r = u;
     double mg = INFINITY;
     /* First loop, Alg. 2 lines 4-11. */
@@ -427,7 +436,7 @@ static int run_one(const orc_circuit* c, uint64_t seed, uint64_t traj,
             int chosen = -1, branch = -1;
             double margin = INFINITY;
             status = sample_channel(psi, n, c->nq[op], qs, c->n_kraus[op],
-                                    mats + c->mat_off[op], u, &chosen, &branch,
+                                    mats + c->mat_off[op], u, c->mode, &chosen, &branch,
                                     &margin);
             if (o->kraus_choice) o->kraus_choice[ch] = chosen;
             if (o->branch) o->branch[ch] = (int8_t)branch;
@@ -502,13 +511,14 @@ int orc_run_trajectories(
     const int* n_kraus, const int64_t* mat_off, const double* mats,
     const double* p00, const double* p11, int n_obs, const char* obs,
     uint64_t seed, uint64_t traj_begin, uint64_t stride, int64_t traj_count,
-    int shots, int n_threads,
+    int shots, int n_threads, int mode,
     double* final_states, int32_t* kraus_choice, int8_t* branch,
     double* kraus_margin, uint64_t* bits, uint64_t* bits_raw,
     double* sample_margin, double* obs_values, int32_t* status) {
     if (n < 1 || n > 30 || n_ops < 0 || shots < 0 || traj_count < 0) return ORC_EINVAL;
+    if (mode != 0 && mode != 1) return ORC_EINVAL;
     orc_circuit c = {n, n_ops, kind, nq, qubits, n_kraus, mat_off, mats,
-                     p00, p11, n_obs, obs};
+                     p00, p11, n_obs, obs, mode};
     int n_channels = 0;
     for (int i = 0; i < n_ops; ++i) n_channels += (kind[i] == 1);
     job_t J;

@@ -345,6 +345,7 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
             }
             po.mixture = mixture;
             if (!mixture) P.max_conv_d = std::max(P.max_conv_d, d);
+            P.max_chan_d = std::max(P.max_chan_d, d);
             if (!mixture && hop->nq > 2) {
                 delete hp;
                 return fail(QT_EARITY, "non-unitary-mixture channels on more than 2 qubits are not supported by the device choose step");

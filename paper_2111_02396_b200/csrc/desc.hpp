@@ -55,7 +55,10 @@ struct EventDesc {
     int32_t record;       // index into the record array, or -1
     int32_t slot;         // batch slot of the trajectory
     double r;             // remaining uniform after the first loop
+    int32_t flags;        // kEventNoBounds: conventional algorithm, pbar_i = 0
+    int32_t pad;
 };
+constexpr int32_t kEventNoBounds = 1;
 
 // Channel data for the device choose step (fp64 in chan_data):
 //   pbar[n_kraus], then M_i = K_i^dag K_i (2*d*d doubles each), then K_i.

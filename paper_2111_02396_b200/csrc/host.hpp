@@ -74,6 +74,7 @@ struct Plan {
     int n_channels = 0;
     int n_recorded = 0;
     int max_conv_d = 1;             // largest d of a non-mixture channel
+    int max_chan_d = 1;             // largest d of any channel (conventional mode)
     std::vector<double> p00, p11;
     bool has_p00 = false, has_p11 = false;
 };
@@ -113,8 +114,9 @@ struct ObsGroups {
 
 // Build the program of trajectory `traj` (Alg. 2 first loop on the host,
 // fusion, tile passes, epilogues).  Returns QT_OK or an error status.
+// mode 0 = Alg. 2 (delayed inner products), 1 = conventional algorithm.
 qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj,
-                          const ObsGroups& og, TrajProgram& out);
+                          const ObsGroups& og, TrajProgram& out, int mode = 0);
 
 // Paper's two-phase fuser on a list of items (exposed for tests).
 struct FuseItem {

@@ -291,8 +291,9 @@ void gate_layout(uint64_t gate_mask, uint64_t S, int T, int R, uint32_t& rpos, u
 }  // namespace
 
 qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const ObsGroups& og,
-                          TrajProgram& out) {
+                          TrajProgram& out, int mode) {
     out = TrajProgram();
+    const bool conventional = (mode == 1);  // no lower bounds, every channel reduces
     const int n = P.n;
     const int T = P.T;
     out.records.assign(P.n_recorded, -1);
@@ -309,11 +310,13 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
         const double u = draw(seed, (uint32_t)op.chan, kPurposeChannel, traj, 0);
         double r = u;
         int pick = -1;
-        for (int i = 0; i < op.n_kraus; ++i) {
-            if (r < op.pbar[i]) { pick = i; break; }
-            r -= op.pbar[i];
+        if (!conventional) {
+            for (int i = 0; i < op.n_kraus; ++i) {
+                if (r < op.pbar[i]) { pick = i; break; }
+                r -= op.pbar[i];
+            }
+            if (pick < 0 && op.mixture) pick = op.n_kraus - 1;  // s == 1
         }
-        if (pick < 0 && op.mixture) pick = op.n_kraus - 1;  // s == 1
         if (pick >= 0) {
             ++out.n_deferred;
             if (op.record >= 0) out.records[op.record] = pick;
@@ -329,6 +332,8 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
         E.record = op.record;
         E.slot = 0;
         E.r = r;
+        E.flags = conventional ? kEventNoBounds : 0;
+        E.pad = 0;
         const int ev = (int)out.events.size();
         out.events.push_back(E);
         barriers.push_back(Barrier{ev, op.mask});

@@ -337,7 +337,8 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
     QT_CK(B.pool.ensure(sizeof(float2) * std::max<int32_t>(pool, 2)));
     QT_CK(B.status.ensure(sizeof(int32_t) * nslots));
     QT_CK(B.counters.ensure(sizeof(int32_t) * nslots));
-    const int rho_stride = 2 * P.max_conv_d * P.max_conv_d;
+    const int rd = std::min(P.max_chan_d, 4);  // conventional mode reduces every channel (q <= 2)
+    const int rho_stride = 2 * rd * rd;
     QT_CK(B.rho_part.ensure(sizeof(double) * (size_t)nslots * ntiles * rho_stride));
     QT_CK(B.blocksum.ensure(sizeof(double) * (size_t)nslots * ntiles));
     QT_CK(B.obs_part.ensure(sizeof(double) * (size_t)nslots * ntiles * std::max(n_obs, 1)));
@@ -526,7 +527,9 @@ qt_status qt_run_trajectories(qt_ctx ctx, qt_plan plan, const qt_run_opts* opts,
                               double* out_obs, qt_stats* out_stats) {
     if (!ctx || !plan || !opts || !state_dev) return fail(QT_EINVAL, "NULL argument");
     if (n_obs < 0 || (n_obs > 0 && !obs)) return fail(QT_EINVAL, "bad observables");
-    if (opts->mode != 0) return fail(QT_EINVAL, "only mode 0 (delayed inner product) is implemented");
+    if (opts->mode != 0 && opts->mode != 1) return fail(QT_EINVAL, "mode must be 0 (delayed) or 1 (conventional)");
+    if (opts->mode == 1 && plan_of(plan).max_chan_d > 4)
+        return fail(QT_EARITY, "conventional mode reduces every channel: channels on more than 2 qubits are not supported");
     if (opts->shots_per_traj < 0) return fail(QT_EINVAL, "shots_per_traj < 0");
     const Plan& P = plan_of(plan);
     QT_CK(cudaSetDevice(ctx->device));
@@ -573,7 +576,8 @@ qt_status qt_run_trajectories(qt_ctx ctx, qt_plan plan, const qt_run_opts* opts,
         for (int b = 0; b < ns; ++b) trajs[b] = opts->traj_begin + (j0 + b) * stride;
         std::vector<qt_status> pst(ns, QT_OK);
         const auto h0 = std::chrono::steady_clock::now();
-        parallel_for(ns, threads, [&](int b) { pst[b] = plan_trajectory(P, opts->seed, trajs[b], og, progs[b]); });
+        parallel_for(ns, threads,
+                     [&](int b) { pst[b] = plan_trajectory(P, opts->seed, trajs[b], og, progs[b], opts->mode); });
         plan_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
         for (int b = 0; b < ns; ++b)
             if (pst[b] != QT_OK) status = pst[b];

@@ -260,8 +260,9 @@ static __device__ __noinline__ void choose_conventional(const EventDesc& E, cons
             }
         raw[i] = s;
         const double p = s / tr;
-        if (p < pbar[i] - 1e-6) { *status = -5; return; }
-        w[i] = p - pbar[i] > 0.0 ? p - pbar[i] : 0.0;
+        const double pb = (E.flags & kEventNoBounds) ? 0.0 : pbar[i];  // conventional algorithm: no bounds
+        if (p < pb - 1e-6) { *status = -5; return; }
+        w[i] = p - pb > 0.0 ? p - pb : 0.0;
         if (r < w[i]) { pick = i; break; }
         r -= w[i];
     }

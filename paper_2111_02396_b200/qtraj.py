@@ -240,11 +240,11 @@ class Context:
     def run_trajectories(self, plan: Plan, state, seed: int, traj_count: int, traj_begin: int = 0,
                          traj_stride: int = 1, shots: int = 1, batch: int = 0,
                          observables: Sequence[str] = (), profile: bool = False,
-                         host_threads: int = 0, want_kraus: bool = True) -> dict:
+                         host_threads: int = 0, want_kraus: bool = True, mode: int = 0) -> dict:
         """state: torch complex64 CUDA tensor with >= 2^n elements per slot."""
         import torch
         assert state.is_cuda and state.dtype == torch.complex64 and state.is_contiguous()
-        o = RunOpts(seed, traj_begin, traj_stride, traj_count, shots, batch, 0, int(profile), host_threads)
+        o = RunOpts(seed, traj_begin, traj_stride, traj_count, shots, batch, mode, int(profile), host_threads)
         bits = np.zeros((traj_count, max(shots, 0)), np.uint64)
         kraus = np.zeros((traj_count, plan.num_recorded), np.int32) if want_kraus else None
         obs = np.zeros((traj_count, len(observables)), np.float64)

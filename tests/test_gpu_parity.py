@@ -92,9 +92,10 @@ def test_all_placements_n10_k2(ctx):
 # ---------------------------------------------------------------------------
 # Trajectories (Alg. 2) vs the oracle, element by element
 # ---------------------------------------------------------------------------
-def run_both(ctx, c, seed, T, shots=1, f=4, batch=0, one_gate=False, traj_begin=0, stride=1, tensor_cores=0):
+def run_both(ctx, c, seed, T, shots=1, f=4, batch=0, one_gate=False, traj_begin=0, stride=1, tensor_cores=0,
+             mode=0):
     ref = oracle.run_trajectories(c, seed=seed, traj_begin=traj_begin, stride=stride, traj_count=T,
-                                  shots=shots, want_states=True)
+                                  shots=shots, want_states=True, mode=mode)
     assert ref["rc"] == 0
     plan = qtraj.Plan(qtraj.Circuit.from_description(c), max_fused=f, one_gate_per_pass=one_gate,
                       tensor_cores=tensor_cores)
@@ -102,7 +103,8 @@ def run_both(ctx, c, seed, T, shots=1, f=4, batch=0, one_gate=False, traj_begin=
         batch = T  # one batch: the state buffer then holds every final state
     state = torch.zeros(batch << c.n_qubits, dtype=torch.complex64, device="cuda")
     out = ctx.run_trajectories(plan, state, seed=seed, traj_count=T, traj_begin=traj_begin,
-                               traj_stride=stride, shots=shots, batch=batch, observables=c.observables)
+                               traj_stride=stride, shots=shots, batch=batch, observables=c.observables,
+                               mode=mode)
     torch.cuda.synchronize()
     return ref, out, state
 
@@ -157,6 +159,17 @@ def test_tensor_core_and_cuda_core_paths(ctx, n, tensor_cores):
                                  t1_ns=700.0, tphi_ns=1200.0, readout=True)
     ref, out, state = run_both(ctx, c, seed=17, T=10, shots=2, tensor_cores=tensor_cores)
     compare(ref, out, state)
+
+
+@pytest.mark.parametrize("n", [5, 12])
+def test_conventional_mode_parity(ctx, n):
+    """NEXT-1: the conventional trajectory algorithm -- every channel is
+    reduced on the device -- against the oracle's conventional mode."""
+    c = workloads.random_circuit(n, depth=5, seed=400 + n, noise="both", p=0.03, t1_ns=900.0, tphi_ns=1500.0,
+                                 readout=True)
+    ref, out, state = run_both(ctx, c, seed=5, T=6, shots=2, mode=1)
+    compare(ref, out, state)
+    assert out["stats"]["reductions"] == 6 * c.n_channels
 
 
 @pytest.mark.parametrize("f", [2, 3, 4, 5, 6])

@@ -375,3 +375,31 @@ def test_estimator_stderr_scaling():
     se_big = v.std(ddof=1) / np.sqrt(10000)
     se_small = v[:100].std(ddof=1) / np.sqrt(100)
     assert 0.066 <= se_big / se_small <= 0.15
+
+
+# --------------------------------------------------------------------------
+# Conventional trajectory algorithm (NEXT-1): same distribution as Alg. 2
+# --------------------------------------------------------------------------
+def test_conventional_mode_matches_density_matrix():
+    n = 4
+    c = workloads.random_circuit(n, depth=5, seed=23, noise="both", p=0.06, t1_ns=500.0, tphi_ns=900.0)
+    c.observables = ["ZIII", "IZII", "XXII", "IYYI", "ZZZZ"]
+    R = 6000
+    r = oracle.run_trajectories(c, seed=78, traj_count=R, shots=1, mode=1)
+    assert r["rc"] == 0
+    assert (r["branch"] == 1).all()  # every channel computes its probabilities
+    rho = dm.evolve(c)
+    for k, s in enumerate(c.observables):
+        v = r["obs"][:, k]
+        se = v.std(ddof=1) / np.sqrt(R)
+        assert abs(v.mean() - dm.expectation(rho, s)) < 4 * se + 1e-9
+
+
+def test_conventional_mode_kraus_frequencies():
+    # depolarizing is a unitary mixture: in conventional mode it is sampled by p_i
+    c = Circuit(1, [[Gate((0,), gates.H())], [Channel((0,), channels.depolarize(0.3))]])
+    R = 60000
+    r = oracle.run_trajectories(c, seed=8, traj_count=R, shots=0, mode=1)
+    counts = np.bincount(r["kraus"][:, 0], minlength=4)
+    exp = np.array([0.7, 0.1, 0.1, 0.1]) * R
+    assert (((counts - exp) ** 2) / exp).sum() < 11.34  # chi-square 3 dof, alpha = 0.01

@@ -234,11 +234,13 @@ def low_noise_grid(rows: int = 2, cols: int = 13, cycles: int = 20, config: int 
             prev[q] = k
             m1.append(Gate((q,), one_q[k]))
         c.moments.append(m1)
-        c.moments.append([Channel((q,), channels.depolarize(depol)) for q in range(n)])
+        if depol > 0:
+            c.moments.append([Channel((q,), channels.depolarize(depol)) for q in range(n)])
         c.moments.append([Channel((q,), channels.phase_damp(gamma_pd)) for q in range(n)])
         pairs = pats[order[cyc % len(order)]]
         c.moments.append([Gate(pr, fsim, "fSim") for pr in pairs])
-        c.moments.append([Channel(pr, channels.depolarize2(depol)) for pr in pairs])
+        if depol > 0:
+            c.moments.append([Channel(pr, channels.depolarize2(depol)) for pr in pairs])
         c.moments.append([Channel((q,), channels.phase_damp(gamma_pd)) for q in range(n)])
     c.observables = ["I" * q + "Z" + "I" * (n - q - 1) for q in range(n)]
     return c
