@@ -288,15 +288,19 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
     P.one_gate = o.one_gate_per_pass != 0;
     // tensor cores: every fused gate padded to 4 qubits (f <= 4), T = 12, 128-thread CTAs
     // whose CUDA-core gates use R = 5
-    const bool tc_ok = (P.T == 12 && f <= 4 && max_arity <= 4);
+    const bool tc_ok = (P.T == 12 && f <= 5 && max_arity <= f);
     if (o.tensor_cores > 0 && !tc_ok) {
         delete hp;
-        return fail(QT_EINVAL, "tensor_cores needs n >= 12, max_fused <= 4 and gates of <= 4 qubits");
+        return fail(QT_EINVAL, "tensor_cores needs n >= 12, max_fused <= 5 and gates of <= max_fused qubits");
     }
     P.tc = o.tensor_cores >= 0 && tc_ok;
     if (P.tc) {
-        P.R = 5;  // 128-thread CTAs (4 per SM), two 16-amplitude subvectors per thread
+        // 128-thread CTAs: f <= 4 -> gates padded to 4 qubits (two 16-amplitude
+        // subvectors per thread, 4 CTAs / SM); f = 5 -> padded to 5 qubits (one
+        // 32-amplitude subvector per thread, 2 CTAs / SM)
+        P.R = 5;
         P.f = f;
+        P.tc_k = f <= 4 ? 4 : 5;
     }
     // canonical order: moment ascending, then call order (stable)
     std::vector<const HostOp*> order;

@@ -43,10 +43,9 @@ struct GateDesc {
 // Largest number of fused gates in one pass (descriptors staged in smem).
 constexpr int kMaxPassGates = 256;
 
-// GateDesc::k / FusedDesc::k flag: a 4-qubit gate applied on tensor cores whose
-// pool entry is the tf32 hi/lo GEMM operand W (tc_common.cuh), 8 KB.
+// GateDesc::k / FusedDesc::k flag: a (4- or 5-qubit padded) gate applied on
+// tensor cores whose pool entry is the tf32 hi/lo GEMM operand W (tc_common.cuh).
 constexpr int32_t kGateTC = 0x100;
-constexpr int32_t kGateTCPoolEntries = 1024;  // complex64 units of one W hi/lo entry
 
 // A conventional channel occurrence (Alg. 2 lines 12-21).
 struct EventDesc {

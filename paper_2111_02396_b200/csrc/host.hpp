@@ -64,7 +64,8 @@ struct Plan {
     int CL = 4;         // low qubits always in a tile
     int R = 4;          // register bits (2^R amplitudes / thread)
     bool one_gate = false;
-    bool tc = false;    // fused gates padded to 4 qubits and applied on tcgen05 tensor cores
+    bool tc = false;    // fused gates padded to tc_k qubits and applied on tcgen05 tensor cores
+    int tc_k = 4;       // 4 (f <= 4) or 5 (f = 5)
     std::vector<PlanOp> ops;
     std::vector<Variant> vars;
     std::vector<VarDesc> var_desc;

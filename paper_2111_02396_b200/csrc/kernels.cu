@@ -33,15 +33,16 @@ namespace qt {
 cudaError_t launch_tile_pass_r4(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s);
 cudaError_t launch_tile_pass_r5(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s);
 cudaError_t launch_tile_pass_r6(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s);
-cudaError_t launch_tile_pass_tc(const TileArgs& a, int R, int step, uint32_t ntiles, int nslots, cudaStream_t s);
+cudaError_t launch_tile_pass_tc(const TileArgs& a, int tck, int step, uint32_t ntiles, int nslots, cudaStream_t s);
 
-size_t tile_pass_smem_bytes(int T, int R, bool tcm) { return tile_pass_smem_bytes_impl(T, R, tcm); }
+size_t tile_pass_smem_bytes(int T, int R, int tck) { return tile_pass_smem_bytes_impl(T, R, tck != 0, tck ? tck : 4); }
 
-cudaError_t launch_tile_pass(const TileArgs& a, int R, bool tcm, int step, uint32_t ntiles, int nslots,
+cudaError_t launch_tile_pass(const TileArgs& a, int R, int tck, int step, uint32_t ntiles, int nslots,
                              cudaStream_t s) {
     // Instantiated (T, R): (12, 4), (12, 5), (12, 6) and (T, min(T, 4)) for
-    // T = 1..11 (the whole state of n < 12 qubits in one CTA); tensor cores: (12, 5).
-    if (tcm) return a.T == 12 ? launch_tile_pass_tc(a, R, step, ntiles, nslots, s) : cudaErrorInvalidValue;
+    // T = 1..11 (the whole state of n < 12 qubits in one CTA); tensor cores
+    // (tck = 4 or 5 qubits per padded gate): (12, 5).
+    if (tck) return a.T == 12 && R == 5 ? launch_tile_pass_tc(a, tck, step, ntiles, nslots, s) : cudaErrorInvalidValue;
     if (a.T == 12 && R == 6) return launch_tile_pass_r6(a, step, ntiles, nslots, s);
     if (a.T == 12 && R == 5) return launch_tile_pass_r5(a, step, ntiles, nslots, s);
     if (R == (a.T < 4 ? a.T : 4)) return launch_tile_pass_r4(a, step, ntiles, nslots, s);
@@ -104,6 +105,8 @@ materialize_kernel(const FusedDesc* __restrict__ fused, const ConsDesc* __restri
     // tensor-core operand W (tc_common.cuh): W[2c + a][2j + b] = real 2x2 block of
     // U[j][c], stored K-major swizzled as hi then lo tf32 parts.  Column c of U = v.
     uint32_t* W = reinterpret_cast<uint32_t*>(pool + F.mat_off);
+    const int k = F.k & 0xff;
+    const uint32_t part = (uint32_t)tc::w_part_bytes(k) >> 2;
     for (int j = 0; j < D; ++j) {
         const double ur = v[j].x, ui = v[j].y;
         const double blk[2][2] = {{ur, ui}, {-ui, ur}};
@@ -112,9 +115,9 @@ materialize_kernel(const FusedDesc* __restrict__ fused, const ConsDesc* __restri
                 const float w = (float)blk[a][b];
                 const uint32_t h = tc::tf32_rna(w);
                 const uint32_t l = tc::tf32_rna(w - __uint_as_float(h));
-                const uint32_t off = tc::w_offset_bytes(2 * j + b, 2 * c + a) >> 2;
+                const uint32_t off = tc::w_offset_bytes_k(k, 2 * j + b, 2 * c + a) >> 2;
                 W[off] = h;
-                W[(tc::kWBytes >> 2) + off] = l;
+                W[part + off] = l;
             }
     }
 }

@@ -30,14 +30,16 @@ struct TileArgs {
     double* obs_part;           // [slot][tile][n_obs]
     int n_obs;
     const ObsDesc* obs;
+    uint32_t prefetch;          // L2-prefetch the tile this many CTAs ahead (0 = off; set by the launcher)
 };
 
 // Largest register width R (amplitudes per thread = 2^R) compiled.
 constexpr int kMaxR = 6;
 constexpr int kMaxT = 12;
 
-size_t tile_pass_smem_bytes(int T, int R, bool tcm);
-cudaError_t launch_tile_pass(const TileArgs& a, int R, bool tcm, int step, uint32_t ntiles, int nslots,
+size_t tile_pass_smem_bytes(int T, int R, int tck);
+// tck: 0 = CUDA-core fused gates; 4 / 5 = tensor-core gates padded to tck qubits.
+cudaError_t launch_tile_pass(const TileArgs& a, int R, int tck, int step, uint32_t ntiles, int nslots,
                              cudaStream_t s);
 
 cudaError_t launch_materialize(const FusedDesc* fused, int n_fused, const ConsDesc* cons,

@@ -414,9 +414,10 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
                     // qubits it does not touch (always inside the tile)
                     uint64_t pm = g.mask;
                     if (P.tc)
-                        for (int q = 0; q < n && popc(pm) < 4; ++q) pm |= 1ull << q;
+                        for (int q = 0; q < n && popc(pm) < P.tc_k; ++q) pm |= 1ull << q;
                     const int d = 1 << popc(pm);
-                    gd.mat_off = alloc(P.tc ? kGateTCPoolEntries : d * d);
+                    // tensor cores: W hi/lo operand, gate_bytes(tc_k) = 2 * (2^(k+1))^2 * 4 B
+                    gd.mat_off = alloc(P.tc ? (2 << P.tc_k) * (2 << P.tc_k) : d * d);
                     FusedDesc fd;
                     fd.mat_off = gd.mat_off;
                     fd.k = popc(pm) | (P.tc ? kGateTC : 0);
@@ -441,7 +442,7 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
                     }
                 }
                 out.alg_flops += std::ldexp(1.0, n + (gd.k & 0xff) + 3);
-                if (P.tc && (gd.k & kGateTC)) gd.k = 4 | kGateTC;
+                if (P.tc && (gd.k & kGateTC)) gd.k = P.tc_k | kGateTC;
                 out.gates.push_back(gd);
                 gate_masks.push_back(g.mask);
             }

@@ -394,12 +394,12 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
             QT_CK(cudaEventCreate(&e0));
             QT_CK(cudaEventCreate(&e1));
             QT_CK(cudaEventRecord(e0, s));
-            QT_CK(launch_tile_pass(A, P.R, P.tc, step, ntiles, nslots, s));
+            QT_CK(launch_tile_pass(A, P.R, P.tc ? P.tc_k : 0, step, ntiles, nslots, s));
             QT_CK(cudaEventRecord(e1, s));
             ctx->prof_ev.push_back(e0);
             ctx->prof_ev.push_back(e1);
         } else {
-            QT_CK(launch_tile_pass(A, P.R, P.tc, step, ntiles, nslots, s));
+            QT_CK(launch_tile_pass(A, P.R, P.tc ? P.tc_k : 0, step, ntiles, nslots, s));
         }
         ++launches;
     }
@@ -692,7 +692,7 @@ static qt_status run_single(qt_ctx ctx, qt_plan plan, float2* state, const ObsGr
     }
     for (int rep = 0; rep < std::max(repeats, 1); ++rep) {
         if (kernel_ms && rep == 1) QT_CK(cudaEventRecord(e0, s));  // rep 0 = warm-up
-        for (int step = 0; step < np; ++step) QT_CK(launch_tile_pass(A, P.R, P.tc, step, ntiles, 1, s));
+        for (int step = 0; step < np; ++step) QT_CK(launch_tile_pass(A, P.R, P.tc ? P.tc_k : 0, step, ntiles, 1, s));
     }
     if (kernel_ms) {
         if (repeats <= 1) QT_CK(cudaEventRecord(e0, s));

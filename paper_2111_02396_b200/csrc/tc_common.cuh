@@ -23,6 +23,20 @@ __host__ __device__ __forceinline__ uint32_t w_offset_bytes(int n, int k) {
 constexpr int kWBytes = 32 * 32 * 4;          // one of hi / lo
 constexpr int kGateBytes = 2 * kWBytes;       // hi then lo (8 KB)
 
+// General k-qubit gate (k = 4, 5): N = K = 2^(k+1).  W is stored as K/32 chunks
+// of [N rows][32 tf32] (each chunk a SWIZZLE_128B K-major block), hi part then lo.
+__host__ __device__ __forceinline__ uint32_t w_offset_bytes_k(int k, int n, int kk) {
+    const int N = 2 << k;
+    return (uint32_t)((kk >> 5) * N * 128) + w_offset_bytes(n, kk & 31);
+}
+__host__ __device__ constexpr int w_part_bytes(int k) { return (2 << k) * (2 << k) * 4; }
+__host__ __device__ constexpr int gate_bytes(int k) { return 2 * w_part_bytes(k); }
+
+// Instruction descriptor: kind::tf32, D f32, A/B tf32 K-major, M = 128, N.
+__host__ __device__ constexpr uint32_t idesc_tf32_m128(int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
+}
+
 // Shared-memory matrix descriptor (K-major, SWIZZLE_128B, SBO = 1024 B).
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t smem_addr) {
     uint64_t d = 0;
@@ -48,6 +62,16 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, ui
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}\n"
         ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(kIdescTf32_M128_N32), "r"(accumulate),
+          "r"(0u), "r"(0u), "r"(0u), "r"(0u));
+}
+
+__device__ __forceinline__ void mma_tf32_ts_n(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                              uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}\n"
+        ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate),
           "r"(0u), "r"(0u), "r"(0u), "r"(0u));
 }
 

@@ -100,57 +100,52 @@ __device__ __forceinline__ void apply_tc_gate(float2* tile, uint32_t w_smem, uin
     fence_before();
 }
 
-// Apply one padded 4-qubit gate on tensor cores with a 256-thread CTA: thread t
-// owns subvector s = t (register bits 0..3 = the gate bits), TMEM lane t & 127,
-// M-group g = t >> 7.  TMEM columns: D_g [32 g, 32 g + 32), A_g hi/lo
-// [64 + 64 g, 96 + 64 g) / [96 + 64 g, 128 + 64 g).  Both groups go in one
-// MMA batch, i.e. one tensor-core round trip per gate.
-__device__ __forceinline__ void apply_tc_gate256(float2* tile, uint32_t w_smem, uint32_t pbase,
-                                                 const uint32_t (&unit)[4], uint32_t tmem, uint64_t* mbar,
-                                                 uint32_t& phase) {
+// Apply one padded 5-qubit gate on tensor cores (128 threads): thread t owns
+// subvector s = t of 32 amplitudes (register bits 0..4 = the gate bits), TMEM
+// lane t.  N = K = 64: TMEM columns D [0,64), A hi [64,128), A lo [128,192);
+// W in shared memory as two K-chunks of [64][32] tf32 (hi, then lo at +16 KB).
+__device__ __forceinline__ void apply_tc_gate5(float2* tile, uint32_t w_smem, uint32_t pbase,
+                                               const uint32_t (&unit)[5], uint32_t tmem, uint64_t* mbar,
+                                               uint32_t& phase) {
     using namespace tc;
     const int tid = threadIdx.x;
-    const int g = tid >> 7;
     char* const tb8 = reinterpret_cast<char*>(tile);
-    uint32_t lo[16];
+    uint32_t lo[32];
     lo[0] = pbase;
 #pragma unroll
-    for (int m = 0; m < 4; ++m)
+    for (int m = 0; m < 5; ++m)
 #pragma unroll
         for (int x = 0; x < (1 << m); ++x) lo[x + (1 << m)] = lo[x] ^ unit[m];
-    const uint32_t lane = (uint32_t)(tid & 96) << 16;  // warp's 32-lane TMEM quarter
-    {
-        // hi = x with the 13 low mantissa bits cleared (exact tf32), lo = x - hi
+    const uint32_t lane = (uint32_t)(tid & 96) << 16;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // configurations 16 h .. 16 h + 15 = A columns 32 h .. 32 h + 31
         uint32_t hi[32], lw[32];
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
-            const float2 v = *reinterpret_cast<const float2*>(tb8 + lo[c]);
+            const float2 v = *reinterpret_cast<const float2*>(tb8 + lo[16 * h + c]);
             const uint32_t hx = __float_as_uint(v.x) & 0xFFFFE000u, hy = __float_as_uint(v.y) & 0xFFFFE000u;
             hi[2 * c] = hx;
             hi[2 * c + 1] = hy;
             lw[2 * c] = __float_as_uint(v.x - __uint_as_float(hx));
             lw[2 * c + 1] = __float_as_uint(v.y - __uint_as_float(hy));
         }
-        tmem_st32(tmem + lane + 64 + 64 * g, hi);
-        tmem_st32(tmem + lane + 96 + 64 * g, lw);
+        tmem_st32(tmem + lane + 64 + 32 * h, hi);
+        tmem_st32(tmem + lane + 128 + 32 * h, lw);
     }
     tmem_wait_st();
     fence_before();
     __syncthreads();
     if (tid == 0) {
         fence_after();
+        constexpr uint32_t idesc = idesc_tf32_m128(64);
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-            const uint64_t bh = smem_desc_sw128(w_smem + ks * 32);
-            const uint64_t bl = smem_desc_sw128(w_smem + kWBytes + ks * 32);
-#pragma unroll
-            for (int gg = 0; gg < 2; ++gg) {
-                const uint32_t d = tmem + 32 * gg;
-                const uint32_t ah = tmem + 64 + 64 * gg + ks * 8, al = ah + 32;
-                mma_tf32_ts(d, ah, bh, ks > 0);
-                mma_tf32_ts(d, al, bh, 1);
-                mma_tf32_ts(d, ah, bl, 1);
-            }
+        for (int ks = 0; ks < 8; ++ks) {
+            const uint32_t off = (uint32_t)((ks >> 2) * 8192 + (ks & 3) * 32);
+            const uint64_t bh = smem_desc_sw128(w_smem + off);
+            const uint64_t bl = smem_desc_sw128(w_smem + (uint32_t)w_part_bytes(5) + off);
+            mma_tf32_ts_n(tmem, tmem + 64 + ks * 8, bh, idesc, ks > 0);
+            mma_tf32_ts_n(tmem, tmem + 128 + ks * 8, bh, idesc, 1);
+            mma_tf32_ts_n(tmem, tmem + 64 + ks * 8, bl, idesc, 1);
         }
         mma_commit(mbar);
     }
@@ -158,20 +153,22 @@ __device__ __forceinline__ void apply_tc_gate256(float2* tile, uint32_t w_smem, 
     mbar_wait(mbar, phase);
     phase ^= 1u;
     fence_after();
-    {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
         uint32_t v[32];
-        tmem_ld32(tmem + lane + 32 * g, v);
+        tmem_ld32(tmem + lane + 32 * h, v);
         tmem_wait_ld();
 #pragma unroll
         for (int c = 0; c < 16; ++c)
-            *reinterpret_cast<float2*>(tb8 + lo[c]) = make_float2(__uint_as_float(v[2 * c]), __uint_as_float(v[2 * c + 1]));
+            *reinterpret_cast<float2*>(tb8 + lo[16 * h + c]) =
+                make_float2(__uint_as_float(v[2 * c]), __uint_as_float(v[2 * c + 1]));
     }
     fence_before();
 }
 
 }  // namespace detail
 
-template <int T, int R, bool TC>
+template <int T, int R, bool TC, int TCK = 4>
 struct TileCfg {
     static constexpr int NT = 1 << (T - R);
     static constexpr int NA = 1 << R;
@@ -179,7 +176,7 @@ struct TileCfg {
     static constexpr int CL = T < detail::kCL ? T : detail::kCL;
     static constexpr int NH = TILE >> CL;
     // shared memory: [W/matrix buffers x2][tile][hoff][red][gdesc][mbar], base 1024-aligned
-    static constexpr size_t kMbufBytes = TC ? (size_t)tc::kGateBytes : sizeof(float2) * ((size_t)1 << (2 * R));
+    static constexpr size_t kMbufBytes = TC ? (size_t)tc::gate_bytes(TCK) : sizeof(float2) * ((size_t)1 << (2 * R));
     static constexpr size_t kTileOff = 2 * kMbufBytes;
     static constexpr size_t kHoffOff = kTileOff + sizeof(float2) * TILE;
     static constexpr size_t kRedOff = kHoffOff + sizeof(uint64_t) * ((NH + 1) & ~1);
@@ -188,11 +185,12 @@ struct TileCfg {
     static constexpr size_t kBytes = kMbarOff + 16 + 1024;  // + alignment slack
 };
 
-template <int T, int R, bool TC>
-__global__ void __launch_bounds__(TileCfg<T, R, TC>::NT, TC ? (R == 4 ? 2 : 4) : ((R <= 4 && T == 12) ? QT_MINB : 1))
+template <int T, int R, bool TC, int TCK = 4>
+__global__ void __launch_bounds__(TileCfg<T, R, TC, TCK>::NT,
+                                  TC ? (TCK == 5 ? 2 : 4) : ((R <= 4 && T == 12) ? QT_MINB : 1))
 tile_pass_kernel(const TileArgs A, const int step) {
-    using Cfg = TileCfg<T, R, TC>;
-    constexpr uint32_t kTmemCols = R == 4 ? 256 : 128;
+    using Cfg = TileCfg<T, R, TC, TCK>;
+    constexpr uint32_t kTmemCols = TCK == 5 ? 256 : 128;  // CTAs per SM share 512 columns
     constexpr int NT = Cfg::NT;
     constexpr int NA = Cfg::NA;
     constexpr int CL = Cfg::CL;
@@ -218,7 +216,15 @@ tile_pass_kernel(const TileArgs A, const int step) {
     const int tid = threadIdx.x;
     const int n = A.n;
     const uint64_t nmask = (n >= 64) ? ~0ull : ((1ull << n) - 1ull);
-    const uint64_t base = pdep64((uint64_t)blockIdx.x, nmask & ~P.tile_mask);
+    // tile base index = blockIdx.x with a zero inserted at every tile-qubit
+    // position (ascending), i.e. pdep(blockIdx.x, ~tile_mask) in T steps
+    uint64_t base = blockIdx.x;
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+        const uint64_t low = base & ((1ull << P.tq[i]) - 1ull);
+        base = low | ((base ^ low) << 1);
+    }
+    (void)nmask;
     float2* st = A.state + ((uint64_t)slot << n);
     const int ng = P.gate_count;
 
@@ -246,18 +252,45 @@ tile_pass_kernel(const TileArgs A, const int step) {
         tc::fence_after();
         tmem = s_tmem;
     }
-    // HBM -> shared, asynchronous 8-byte copies: 2^CL-amplitude contiguous runs
+    // warm L2 with the same-slot tile one resident wave ahead (its CTA will load it soon)
+    if (A.prefetch && blockIdx.x + A.prefetch < gridDim.x) {
+        const uint64_t nb = pdep64((uint64_t)(blockIdx.x + A.prefetch), nmask & ~P.tile_mask);
+        for (int h = tid; h < NH; h += NT)
+            asm volatile("prefetch.global.L2 [%0];\n" ::"l"(st + nb + hoff[h]));
+    }
+    // HBM -> shared.  Wide tiles: 16-byte loads of amplitude pairs (thread t owns
+    // pairs p = t + m NT, so lanes cover 8 x 16 B of each 128-byte run), all
+    // issued before the swizzled 8-byte shared stores.  hoff is linear in its
+    // index bits: hoff[(t >> 3) + m NT / 8] = hoff[t >> 3] | hoff[m NT / 8].
+    constexpr bool kWide = (CL == 4) && (NT >= 8) && (NA >= 2) && (NA <= 32);
+    // measured (n = 30 single-gate passes): register-staged 16-byte loads 61% of
+    // HBM peak vs 8-byte cp.async 68% -> loads stay asynchronous; stores are wide
+    constexpr bool kWideLoad = false;
+    if constexpr (kWideLoad) {
+        const float4* gsrc = reinterpret_cast<const float4*>(st + base + hoff[tid >> 3] + 2 * (tid & 7));
+        float4 v[NA / 2];
 #pragma unroll
-    for (int m = 0; m < NA; ++m) {
-        const uint32_t L = (uint32_t)(tid + m * NT);
-        const uint64_t g = base + hoff[L >> CL] + (L & ((1u << CL) - 1u));
-        cp_async8(tile + swz(L), st + g);
+        for (int m = 0; m < NA / 2; ++m) v[m] = __ldcs(gsrc + (hoff[m * (NT / 8)] >> 1));
+#pragma unroll
+        for (int m = 0; m < NA / 2; ++m) {
+            const uint32_t L = 2u * (uint32_t)(tid + m * NT);
+            tile[swz(L)] = make_float2(v[m].x, v[m].y);
+            tile[swz(L + 1)] = make_float2(v[m].z, v[m].w);
+        }
+    } else {
+        // 8-byte asynchronous copies (small tiles)
+#pragma unroll
+        for (int m = 0; m < NA; ++m) {
+            const uint32_t L = (uint32_t)(tid + m * NT);
+            const uint64_t g = base + hoff[L >> CL] + (L & ((1u << CL) - 1u));
+            cp_async8(tile + swz(L), st + g);
+        }
     }
     cp_async_commit();
     cp_async_wait_all();  // gate descriptors (the tile may still be in flight for other threads)
     __syncthreads();
     auto mat_bytes = [](const GateDesc& G) -> int {
-        return (TC && (G.k & kGateTC)) ? tc::kGateBytes : (int)sizeof(float2) * (1 << (2 * (G.k & 0xff)));
+        return (TC && (G.k & kGateTC)) ? tc::gate_bytes(TCK) : (int)sizeof(float2) * (1 << (2 * (G.k & 0xff)));
     };
     if (ng > 0) {
         const int chunks = mat_bytes(gdesc[0]) >> 4;
@@ -289,12 +322,12 @@ tile_pass_kernel(const TileArgs A, const int step) {
         unsigned char* mcur = mbuf + (gi & 1) * Cfg::kMbufBytes;
         if constexpr (TC) {
             if (G.k & kGateTC) {
-                if constexpr (R == 5)
+                if constexpr (R == 5 && TCK == 4)
                     apply_tc_gate(tile, (uint32_t)__cvta_generic_to_shared(mcur), swz(tb) << 3, unit, tmem, mbar,
                                   phase);
-                else if constexpr (R == 4)
-                    apply_tc_gate256(tile, (uint32_t)__cvta_generic_to_shared(mcur), swz(tb) << 3, unit, tmem,
-                                     mbar, phase);
+                else if constexpr (R == 5 && TCK == 5)
+                    apply_tc_gate5(tile, (uint32_t)__cvta_generic_to_shared(mcur), swz(tb) << 3, unit, tmem, mbar,
+                                   phase);
             } else if ((G.k & 0xff) == 1) {  // device-chosen conventional operators (q <= 2)
                 apply_fused<1, R>(tile, reinterpret_cast<const float2*>(mcur), swz(tb) << 3, unit);
             } else {
@@ -401,11 +434,21 @@ tile_pass_kernel(const TileArgs A, const int step) {
 
     // ---- shared -> HBM ----
     if (P.flags & kPassStore) {
+        if constexpr (kWide) {
+            float4* gdst = reinterpret_cast<float4*>(st + base + hoff[tid >> 3] + 2 * (tid & 7));
 #pragma unroll
-        for (int m = 0; m < NA; ++m) {
-            const uint32_t L = (uint32_t)(tid + m * NT);
-            const uint64_t g = base + hoff[L >> CL] + (L & ((1u << CL) - 1u));
-            st[g] = tile[swz(L)];
+            for (int m = 0; m < NA / 2; ++m) {
+                const uint32_t L = 2u * (uint32_t)(tid + m * NT);
+                const float2 a0 = tile[swz(L)], a1 = tile[swz(L + 1)];
+                gdst[hoff[m * (NT / 8)] >> 1] = make_float4(a0.x, a0.y, a1.x, a1.y);
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < NA; ++m) {
+                const uint32_t L = (uint32_t)(tid + m * NT);
+                const uint64_t g = base + hoff[L >> CL] + (L & ((1u << CL) - 1u));
+                st[g] = tile[swz(L)];
+            }
         }
     }
     if constexpr (TC) {
@@ -417,26 +460,36 @@ tile_pass_kernel(const TileArgs A, const int step) {
     }
 }
 
-inline size_t tile_pass_smem_bytes_impl(int T, int R, bool tcm) {
+inline size_t tile_pass_smem_bytes_impl(int T, int R, bool tcm, int tck = 4) {
     const int CL = T < detail::kCL ? T : detail::kCL;
-    const size_t mb = tcm ? (size_t)tc::kGateBytes : sizeof(float2) * ((size_t)1 << (2 * R));
+    const size_t mb = tcm ? (size_t)tc::gate_bytes(tck) : sizeof(float2) * ((size_t)1 << (2 * R));
     const size_t nh = ((((size_t)1 << T) >> CL) + 1) & ~(size_t)1;
     return 2 * mb + (sizeof(float2) << T) + sizeof(uint64_t) * nh + 64 * sizeof(double) +
            sizeof(GateDesc) * kMaxPassGates + 16 + 1024;
 }
 
-template <int T, int R, bool TC>
+template <int T, int R, bool TC, int TCK = 4>
 cudaError_t launch_tr(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s) {
-    const size_t smem = TileCfg<T, R, TC>::kBytes;
+    using Cfg = TileCfg<T, R, TC, TCK>;
+    const size_t smem = Cfg::kBytes;
     static bool configured = false;
+    static uint32_t resident = 0;  // CTAs resident on the whole device
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(tile_pass_kernel<T, R, TC>,
+        cudaError_t e = cudaFuncSetAttribute(tile_pass_kernel<T, R, TC, TCK>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
+        int per_sm = 0, dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_pass_kernel<T, R, TC, TCK>, Cfg::NT, smem);
+        resident = (uint32_t)(per_sm * sms);
         configured = true;
     }
+    TileArgs b = a;
+    b.prefetch = 0;  // measured: L2 prefetch of the next wave's tiles did not help (64% vs 66% of HBM)
+    (void)resident;
     dim3 grid(ntiles, nslots);
-    tile_pass_kernel<T, R, TC><<<grid, TileCfg<T, R, TC>::NT, smem, s>>>(a, step);
+    tile_pass_kernel<T, R, TC, TCK><<<grid, Cfg::NT, smem, s>>>(b, step);
     return cudaGetLastError();
 }
 
