@@ -11,6 +11,12 @@
 #pragma once
 #include "tile_pass.cuh"
 
+// 1: tensor-core gates issue both M-groups in one MMA batch (256 TMEM columns,
+// 2 CTAs / SM); 0: two batches sharing one A buffer (128 columns, 4 CTAs / SM).
+#ifndef QT_TC_ONE_ROUND
+#define QT_TC_ONE_ROUND 0
+#endif
+
 namespace qt {
 
 namespace detail {
@@ -75,6 +81,42 @@ __device__ __forceinline__ void apply_tc_gate(float2* tile, uint32_t w_smem, uin
             *reinterpret_cast<float2*>(tb8 + (b ^ lo[c])) =
                 make_float2(__uint_as_float(v[2 * c]), __uint_as_float(v[2 * c + 1]));
     };
+#if QT_TC_ONE_ROUND
+    // variant: both groups' A in TMEM (A_g hi/lo at [64 + 64 g, 128 + 64 g)),
+    // one MMA batch and one round trip per gate; needs 256 TMEM columns
+    for (int g = 0; g < 2; ++g) {
+        uint32_t hi[32], lw[32];
+        gather(g, hi, lw);
+        tmem_st32(tmem + lane_off + 64 + 64 * g, hi);
+        tmem_st32(tmem + lane_off + 96 + 64 * g, lw);
+    }
+    tmem_wait_st();
+    fence_before();
+    __syncthreads();
+    if (tid == 0) {
+        fence_after();
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t bh = smem_desc_sw128(w_smem + ks * 32);
+            const uint64_t bl = smem_desc_sw128(w_smem + kWBytes + ks * 32);
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+                mma_tf32_ts(tmem + 32 * g, tmem + 64 + 64 * g + ks * 8, bh, ks > 0);
+                mma_tf32_ts(tmem + 32 * g, tmem + 96 + 64 * g + ks * 8, bh, 1);
+                mma_tf32_ts(tmem + 32 * g, tmem + 64 + 64 * g + ks * 8, bl, 1);
+            }
+        }
+        mma_commit(mbar);
+    }
+    __syncwarp();
+    mbar_wait(mbar, phase);
+    phase ^= 1u;
+    fence_after();
+    scatter(0);
+    scatter(1);
+    fence_before();
+    return;
+#endif
     {
         uint32_t hi[32], lw[32];
         gather(0, hi, lw);
@@ -187,10 +229,10 @@ struct TileCfg {
 
 template <int T, int R, bool TC, int TCK = 4>
 __global__ void __launch_bounds__(TileCfg<T, R, TC, TCK>::NT,
-                                  TC ? (TCK == 5 ? 2 : 4) : ((R <= 4 && T == 12) ? QT_MINB : 1))
+                                  TC ? ((TCK == 5 || QT_TC_ONE_ROUND) ? 2 : 4) : ((R <= 4 && T == 12) ? QT_MINB : 1))
 tile_pass_kernel(const TileArgs A, const int step) {
     using Cfg = TileCfg<T, R, TC, TCK>;
-    constexpr uint32_t kTmemCols = TCK == 5 ? 256 : 128;  // CTAs per SM share 512 columns
+    constexpr uint32_t kTmemCols = (TCK == 5 || QT_TC_ONE_ROUND) ? 256 : 128;  // CTAs per SM share 512 columns
     constexpr int NT = Cfg::NT;
     constexpr int NA = Cfg::NA;
     constexpr int CL = Cfg::CL;
