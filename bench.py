@@ -31,6 +31,7 @@ sys.path.insert(0, ROOT)
 import workloads  # noqa: E402
 
 CONFIG = 2
+TENSOR_CORES = 0  # qt_fuse_opts.tensor_cores (set from --tensor-cores)
 TOTAL_TRAJ = 10_000
 N_QUBITS = 20
 METRIC = "noisy trajectories/s (C2: 20q Sycamore-style depth-14, approximate QCS noise)"
@@ -147,7 +148,7 @@ def bench_reference(args):
 def build_plan(circ, f):
     from paper_2111_02396_b200 import qtraj
     c = qtraj.Circuit.from_description(circ)
-    return c, qtraj.Plan(c, max_fused=f)
+    return c, qtraj.Plan(c, max_fused=f, tensor_cores=TENSOR_CORES)
 
 
 def circuit_bytes(circ):
@@ -281,7 +282,11 @@ def bench_gpu(args):
     fp32_peak_tf = 148 * 128 * 2 * mhz * 1e6 / 1e12  # B200: 148 SMs x 128 FP32 lanes x FMA, at the sampled clock
     frac_hbm = achieved_gbs / hbm_peak
     frac_alu = achieved_tf / fp32_peak_tf
-    if frac_alu > frac_hbm:
+    # With the tensor-core K1 (default for f <= 5) the fused-gate arithmetic is not
+    # on the FP32 pipes; the pass is then reported against its HBM roofline (every
+    # pass must move 2^(n+4) bytes).  The CUDA-core K1 reports the larger
+    # of its FP32-issue and HBM fractions.
+    if frac_alu > frac_hbm and not args.tensor_cores_on:
         roof = {"bound": "alu", "achieved": achieved_tf, "peak": fp32_peak_tf, "unit": "TFLOP/s",
                 "frac": frac_alu, "traffic": None,
                 "peak_source": f"derived: 148 SM x 128 FP32 lanes x 2 flop x {mhz:.0f} MHz (sampled)",
@@ -300,7 +305,8 @@ def bench_gpu(args):
         roof["traffic_unit"] = "bytes/launch"
         roof["traffic_source"] = tr["source"]
     roof["alg_bytes_per_launch"] = alg_bytes / max(pass_launches, 1)
-    roof["kernel"] = "tile_pass_kernel<12,4>"
+    roof["kernel"] = ("tile_pass_kernel<12,5,tensor-core,%d>" % (4 if args.fuse <= 4 else 5)
+                      if args.tensor_cores_on else "tile_pass_kernel<12,4> (CUDA cores)")
     roof["launches_timed"] = int(pass_launches)
     roof["avg_launch_ms"] = pass_ms / max(pass_launches, 1)
     roof["share_of_step"] = pass_ms / tot_ms if tot_ms else None
@@ -358,10 +364,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--fuse", type=int, default=4)
+    ap.add_argument("--tensor-cores", type=int, default=0, help="0 auto, 1 on, -1 CUDA-core K1")
     ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sweep-n", type=int, default=30, help="qubits of the gate-pass bandwidth sweep (0 = skip)")
     args = ap.parse_args()
+    global TENSOR_CORES
+    TENSOR_CORES = args.tensor_cores
+    args.tensor_cores_on = args.tensor_cores >= 0 and args.fuse <= 5  # n = 20 >= 12: auto enables them
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

@@ -190,6 +190,30 @@ qt_status qt_sample_bitstrings(qt_ctx ctx, const void* state_dev, int n, uint64_
 qt_status qt_expectation_value(qt_ctx ctx, const void* state_dev, int n, int n_obs,
                                const qt_pauli* obs, double* out);
 
+/* ---- building blocks of the distributed-state mode ------------
+ * A state of n_total = n + g qubits is split over 2^g processes (global index =
+ * rank << n | local index); gates act on local qubits, global qubits are
+ * swapped in by an all-to-all (paper_2111_02396_b200/distributed.py).
+ * qt_add_matrix: like qt_add_gate without the unitarity check (deferred
+ *   non-unitary Kraus operators, K_i / sqrt(p_i) of conventional picks).
+ * qt_apply_plan: apply every operation of a gate-only plan to a caller state
+ *   (2^n amplitudes, in place); QT_EINVAL if the plan holds channels.
+ * qt_reduce_rho: rho_Q[a][b] = sum_rest psi[rest,a] conj(psi[rest,b]) over the
+ *   local qubits qubits[0..nq) (nq <= 2), fp64, fixed summation order; out =
+ *   2 * 4^nq doubles, row-major interleaved, index bit m <-> m-th lowest qubit.
+ * qt_sample_local: the chain-rule levels n-1..0 of shots shot_ids[0..nshots)
+ *   of a register of n_total qubits whose high bits were already sampled (RNG
+ *   ordinals use n_total); out[i] = the n low bits, no readout error.
+ * qt_expectation_partials: <psi|P|psi>/<psi|psi> of the local state and
+ *   out_norm = <psi|psi>, so ranks can combine sum_r norm_r * value_r. */
+qt_status qt_add_matrix(qt_circuit c, int moment, int nq, const int* qubits, const double* M);
+qt_status qt_apply_plan(qt_ctx ctx, qt_plan plan, void* state_dev, size_t state_bytes);
+qt_status qt_reduce_rho(qt_ctx ctx, const void* state_dev, int n, int nq, const int* qubits, double* out);
+qt_status qt_sample_local(qt_ctx ctx, const void* state_dev, int n, int n_total, uint64_t seed, uint64_t traj,
+                          int nshots, const int32_t* shot_ids, uint64_t* out);
+qt_status qt_expectation_partials(qt_ctx ctx, const void* state_dev, int n, int n_obs, const qt_pauli* obs,
+                                  double* out, double* out_norm);
+
 /* Host-only introspection of the planner (no device work): plans trajectory
  * `traj` exactly as qt_run_trajectories would and reports
  * out[0] tile passes, [1] fused gates, [2] conventional channels (rho_Q

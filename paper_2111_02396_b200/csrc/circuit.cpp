@@ -197,6 +197,28 @@ qt_status qt_add_gate(qt_circuit c, int moment, int nq, const int* qubits, const
     return QT_OK;
 }
 
+qt_status qt_add_matrix(qt_circuit c, int moment, int nq, const int* qubits, const double* M) {
+    if (!c || !M) return fail(QT_EINVAL, "NULL argument");
+    uint64_t mask;
+    qt_status st = check_qubits(c, moment, nq, qubits, &mask);
+    if (st != QT_OK) return st;
+    HostOp op;
+    op.kind = 0;
+    op.moment = moment;
+    op.seq = c->c.seq++;
+    op.nq = nq;
+    op.mask = mask;
+    op.n_kraus = 1;
+    const int d = 1 << nq;
+    op.mats.resize((size_t)d * d);
+    canonicalize(nq, qubits, M, op.q, op.mats.data());
+    for (const cd& x : op.mats)
+        if (!std::isfinite(x.real()) || !std::isfinite(x.imag())) return fail(QT_EINVAL, "non-finite matrix entry");
+    c->moment_mask[moment] |= mask;
+    c->c.ops.push_back(std::move(op));
+    return QT_OK;
+}
+
 qt_status qt_add_channel(qt_circuit c, int moment, int nq, const int* qubits, int n_kraus,
                          const double* K, int record) {
     if (!c || !K) return fail(QT_EINVAL, "NULL argument");

@@ -177,14 +177,16 @@ __global__ void __launch_bounds__(128)
 sample_kernel(const float2* __restrict__ state, int n, int T, const double* __restrict__ blocksum,
               int nslots, int shots, uint64_t seed, const uint64_t* __restrict__ traj_ids,
               const double* __restrict__ p00, const double* __restrict__ p11,
-              uint64_t* __restrict__ out_bits) {
+              uint64_t* __restrict__ out_bits, int n_rng, const int32_t* __restrict__ shot_ids) {
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (gw >= nslots * shots) return;
     const int slot = gw / shots;
-    const int shot = gw % shots;
+    // distributed-state sampling: shot ids and the RNG's qubit count are the
+    // whole register's (the local levels are its low n qubits)
+    const int shot = shot_ids ? shot_ids[gw % shots] : gw % shots;
     const uint64_t traj = traj_ids[slot];
-    const int half_n = (n + 1) / 2;
+    const int half_n = ((n_rng > 0 ? n_rng : n) + 1) / 2;
     const uint64_t ntiles = 1ull << (n - T);
     const double* bs = blocksum + (uint64_t)slot * ntiles;
     uint64_t lo = 0;  // prefix (tile index range [lo, lo + 2^(l-T+1)))
@@ -247,13 +249,106 @@ sample_kernel(const float2* __restrict__ state, int n, int T, const double* __re
 
 cudaError_t launch_sample(const float2* state, int n, int T, const double* blocksum, int nslots,
                           int shots, uint64_t seed, const uint64_t* traj_ids, const double* p00,
-                          const double* p11, uint64_t* out_bits, cudaStream_t s) {
+                          const double* p11, uint64_t* out_bits, cudaStream_t s, int n_rng,
+                          const int32_t* shot_ids) {
     const long warps = (long)nslots * shots;
     if (warps <= 0) return cudaSuccess;
     const int threads = 128;
     const long blocks = (warps * 32 + threads - 1) / threads;
     sample_kernel<<<(unsigned)blocks, threads, 0, s>>>(state, n, T, blocksum, nslots, shots, seed,
-                                                       traj_ids, p00, p11, out_bits);
+                                                       traj_ids, p00, p11, out_bits, n_rng, shot_ids);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// rho_Q of a few local qubits over a whole state (distributed-state mode): fixed
+// grid, fp64 per-block partials, then a fixed-order final sum (deterministic).
+// rho[a][b] = sum_rest psi[rest, a] conj(psi[rest, b]), a/b in internal order
+// (bit m <-> the m-th lowest qubit of qmask).
+// ---------------------------------------------------------------------------
+constexpr int kRhoBlocks = 296;
+
+__global__ void __launch_bounds__(256)
+rho_reduce_kernel(const float2* __restrict__ state, int n, uint64_t qmask, int q, double* __restrict__ partial) {
+    __shared__ double red[8];
+    const int d = 1 << q;
+    uint64_t qoff[4];
+    for (int a = 0; a < d; ++a) {
+        uint64_t o = 0, m = qmask;
+        int bit = 0;
+        while (m) {
+            const uint64_t low = m & (~m + 1);
+            if ((a >> bit) & 1) o |= low;
+            ++bit;
+            m ^= low;
+        }
+        qoff[a] = o;
+    }
+    double acc[32];
+    for (int e = 0; e < 32; ++e) acc[e] = 0.0;
+    const uint64_t total = 1ull << n;
+    for (uint64_t g = (uint64_t)blockIdx.x * 256 + threadIdx.x; g < total; g += (uint64_t)gridDim.x * 256) {
+        if (g & qmask) continue;
+        double vr[4], vi[4];
+        for (int a = 0; a < d; ++a) {
+            const float2 v = state[g | qoff[a]];
+            vr[a] = v.x;
+            vi[a] = v.y;
+        }
+        for (int a = 0; a < d; ++a)
+            for (int b = 0; b < d; ++b) {
+                acc[2 * (a * d + b)] += vr[a] * vr[b] + vi[a] * vi[b];
+                acc[2 * (a * d + b) + 1] += vi[a] * vr[b] - vr[a] * vi[b];
+            }
+    }
+    for (int e = 0; e < 2 * d * d; ++e) {
+        const double s = block_sum<256>(acc[e], red);
+        if (threadIdx.x == 0) partial[(size_t)blockIdx.x * 32 + e] = s;
+    }
+}
+
+__global__ void rho_final_kernel(const double* __restrict__ partial, int ne, double* __restrict__ out) {
+    const int e = threadIdx.x;
+    if (e >= ne) return;
+    double s = 0.0;
+    for (int b = 0; b < kRhoBlocks; ++b) s += partial[(size_t)b * 32 + e];
+    out[e] = s;
+}
+
+// Qubit permutation copy: dst[pi(i)] = src[i], bit j of i moves to bit perm[j]
+// (distributed-state mode: gathers the swapped local qubits into the top bits).
+__global__ void __launch_bounds__(256)
+permute_qubits_kernel(const float2* __restrict__ src, float2* __restrict__ dst, int n, const uint32_t perm_lo,
+                      const uint32_t perm_hi, const uint32_t perm_hh, const uint32_t perm_x) {
+    // perm packed 5 bits per qubit (n <= 34): words lo (q 0..5), hi (6..11), hh (12..17), x (18..23)
+    const uint64_t total = 1ull << n;
+    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < total; i += (uint64_t)gridDim.x * 256) {
+        uint64_t j = 0;
+        for (int b = 0; b < n; ++b) {
+            const uint32_t w = b < 6 ? perm_lo : (b < 12 ? perm_hi : (b < 18 ? perm_hh : perm_x));
+            const int p = (int)((w >> (5 * (b % 6))) & 31u);
+            j |= ((i >> b) & 1ull) << p;
+        }
+        dst[j] = src[i];
+    }
+}
+
+cudaError_t launch_permute_qubits(const float2* src, float2* dst, int n, const int* perm, cudaStream_t s) {
+    if (n > 24) return cudaErrorInvalidValue;
+    uint32_t w[4] = {0, 0, 0, 0};
+    for (int b = 0; b < n; ++b) w[b / 6] |= (uint32_t)perm[b] << (5 * (b % 6));
+    const uint64_t total = 1ull << n;
+    const unsigned blocks = (unsigned)std::min<uint64_t>((total + 255) / 256, 148 * 16);
+    permute_qubits_kernel<<<blocks, 256, 0, s>>>(src, dst, n, w[0], w[1], w[2], w[3]);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rho_reduce(const float2* state, int n, uint64_t qmask, int q, double* partial, double* out,
+                              cudaStream_t s) {
+    rho_reduce_kernel<<<kRhoBlocks, 256, 0, s>>>(state, n, qmask, q, partial);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    rho_final_kernel<<<1, 32, 0, s>>>(partial, 2 << (2 * q), out);
     return cudaGetLastError();
 }
 

@@ -54,6 +54,12 @@ cudaError_t launch_init_states(float2* state, int n, int nslots, cudaStream_t s)
 
 cudaError_t launch_sample(const float2* state, int n, int T, const double* blocksum, int nslots,
                           int shots, uint64_t seed, const uint64_t* traj_ids, const double* p00,
-                          const double* p11, uint64_t* out_bits, cudaStream_t s);
+                          const double* p11, uint64_t* out_bits, cudaStream_t s, int n_rng = 0,
+                          const int32_t* shot_ids = nullptr);
+
+// rho_Q (2^q x 2^q, q <= 2) of the qubits in qmask over a whole n-qubit state;
+// partial: kRhoBlocks x 32 doubles scratch; out: 2 * 4^q doubles (device).
+cudaError_t launch_rho_reduce(const float2* state, int n, uint64_t qmask, int q, double* partial, double* out,
+                              cudaStream_t s);
 
 }  // namespace qt

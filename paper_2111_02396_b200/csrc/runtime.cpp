@@ -619,10 +619,17 @@ qt_status qt_run_trajectories(qt_ctx ctx, qt_plan plan, const qt_run_opts* opts,
 
 // ---- stand-alone state operations -----------------------------------------
 
+// Extra inputs/outputs of the stand-alone path (distributed-state mode).
+struct SingleExtras {
+    double* out_norm = nullptr;        // <psi|psi> of the state (with out_obs)
+    int n_rng = 0;                     // qubits of the whole register for the SAMPLE ordinals
+    const int32_t* shot_ids = nullptr; // host: shot ordinal of each sampled shot
+};
+
 static qt_status run_single(qt_ctx ctx, qt_plan plan, float2* state, const ObsGroups& og,
                             const std::vector<ObsDesc>& obs_table, int n_obs, int shots, uint64_t seed,
                             uint64_t traj, uint64_t* out_bits, double* out_obs, int repeats, double* kernel_ms,
-                            bool zero_state) {
+                            bool zero_state, const SingleExtras* ex = nullptr) {
     const Plan& P = plan_of(plan);
     QT_CK(cudaSetDevice(ctx->device));
     qt_status e = upload_plan_tables(ctx, P, obs_table);
@@ -698,15 +705,24 @@ static qt_status run_single(qt_ctx ctx, qt_plan plan, float2* state, const ObsGr
         if (repeats <= 1) QT_CK(cudaEventRecord(e0, s));
         QT_CK(cudaEventRecord(e1, s));
     }
-    if (out_obs && n_obs > 0)
+    const bool want_norm = ex && ex->out_norm;
+    if ((out_obs && n_obs > 0) || want_norm)
         QT_CK(launch_finalize_obs(B.blocksum.as<double>(), B.obs_part.as<double>(), (int)ntiles, n_obs, 1,
-                                  B.obs_out.as<double>(), nullptr, s));
-    if (out_bits && shots > 0)
+                                  B.obs_out.as<double>(), B.records.as<double>() /* 16 B scratch: norm */, s));
+    int32_t* dshots = nullptr;
+    if (out_bits && shots > 0) {
+        if (ex && ex->shot_ids) {
+            QT_CK(B.counters.ensure(sizeof(int32_t) * std::max(shots, 1)));
+            QT_CK(cudaMemcpyAsync(B.counters.p, ex->shot_ids, sizeof(int32_t) * shots, cudaMemcpyHostToDevice, s));
+            dshots = B.counters.as<int32_t>();
+        }
         QT_CK(launch_sample(state, n, T, B.blocksum.as<double>(), 1, shots, seed, B.traj_ids.as<uint64_t>(), nullptr,
-                            nullptr, B.bits.as<uint64_t>(), s));
+                            nullptr, B.bits.as<uint64_t>(), s, ex ? ex->n_rng : 0, dshots));
+    }
     std::vector<double> obs_host(std::max(n_obs, 1));
     if (out_obs && n_obs > 0)
         QT_CK(cudaMemcpyAsync(obs_host.data(), B.obs_out.p, sizeof(double) * n_obs, cudaMemcpyDeviceToHost, s));
+    if (want_norm) QT_CK(cudaMemcpyAsync(ex->out_norm, B.records.p, sizeof(double), cudaMemcpyDeviceToHost, s));
     if (out_bits && shots > 0)
         QT_CK(cudaMemcpyAsync(out_bits, B.bits.p, sizeof(uint64_t) * shots, cudaMemcpyDeviceToHost, s));
     QT_CK(cudaStreamSynchronize(s));
@@ -806,6 +822,79 @@ qt_status qt_expectation_value(qt_ctx ctx, const void* state_dev, int n, int n_o
     if ((e = parse_obs(n, P.T, P.CL, n_obs, obs, table, og)) == QT_OK)
         e = run_single(ctx, p, const_cast<float2*>(reinterpret_cast<const float2*>(state_dev)), og, table, n_obs, 0,
                        0, 0, nullptr, out, 1, nullptr, false);
+    qt_plan_destroy(p);
+    return e;
+}
+
+// ---- building blocks of the distributed-state mode -------------------------
+
+qt_status qt_apply_plan(qt_ctx ctx, qt_plan plan, void* state_dev, size_t state_bytes) {
+    if (!ctx || !plan || !state_dev) return fail(QT_EINVAL, "NULL argument");
+    const Plan& P = plan_of(plan);
+    if ((sizeof(float2) << P.n) > state_bytes) return fail(QT_EOOM, "state buffer smaller than 2^n amplitudes");
+    for (const PlanOp& op : P.ops)
+        if (op.kind != 0) return fail(QT_EINVAL, "qt_apply_plan: the plan must hold gates/matrices only");
+    ObsGroups og;
+    og.final_pass = false;
+    return run_single(ctx, plan, reinterpret_cast<float2*>(state_dev), og, {}, 0, 0, 0, 0, nullptr, nullptr, 1,
+                      nullptr, false);
+}
+
+qt_status qt_reduce_rho(qt_ctx ctx, const void* state_dev, int n, int nq, const int* qubits, double* out) {
+    if (!ctx || !state_dev || !qubits || !out) return fail(QT_EINVAL, "NULL argument");
+    if (nq < 1 || nq > 2) return fail(QT_EARITY, "qt_reduce_rho: 1 or 2 qubits");
+    uint64_t qmask = 0;
+    for (int i = 0; i < nq; ++i) {
+        if (qubits[i] < 0 || qubits[i] >= n) return fail(QT_EQUBIT, "qubit out of range");
+        qmask |= 1ull << qubits[i];
+    }
+    if (__builtin_popcountll(qmask) != nq) return fail(QT_EQUBIT, "duplicate qubit");
+    QT_CK(cudaSetDevice(ctx->device));
+    BatchBufs& B = ctx->bb[0];
+    if (finish_batch(B, Plan(), 0, 0, CallOut{}) != QT_OK) return QT_ECUDA;
+    QT_CK(B.rho_part.ensure(sizeof(double) * 296 * 32 + sizeof(double) * 32));
+    double* partial = B.rho_part.as<double>();
+    double* dout = partial + 296 * 32;
+    QT_CK(launch_rho_reduce(reinterpret_cast<const float2*>(state_dev), n, qmask, nq, partial, dout, ctx->stream));
+    QT_CK(cudaMemcpyAsync(out, dout, sizeof(double) * (2 << (2 * nq)), cudaMemcpyDeviceToHost, ctx->stream));
+    QT_CK(cudaStreamSynchronize(ctx->stream));
+    return QT_OK;
+}
+
+qt_status qt_sample_local(qt_ctx ctx, const void* state_dev, int n_local, int n_total, uint64_t seed, uint64_t traj,
+                          int nshots, const int32_t* shot_ids, uint64_t* out) {
+    if (!ctx || !state_dev || (nshots > 0 && (!shot_ids || !out)) || nshots < 0 || n_total < n_local)
+        return fail(QT_EINVAL, "bad argument");
+    if (nshots == 0) return QT_OK;
+    qt_plan p = nullptr;
+    qt_status e = read_only_plan(n_local, &p);
+    if (e != QT_OK) return e;
+    ObsGroups og;
+    og.ranges.push_back({0, 0});
+    og.masks.push_back(0);
+    SingleExtras ex;
+    ex.n_rng = n_total;
+    ex.shot_ids = shot_ids;
+    e = run_single(ctx, p, const_cast<float2*>(reinterpret_cast<const float2*>(state_dev)), og, {}, 0, nshots, seed,
+                   traj, out, nullptr, 1, nullptr, false, &ex);
+    qt_plan_destroy(p);
+    return e;
+}
+
+qt_status qt_expectation_partials(qt_ctx ctx, const void* state_dev, int n, int n_obs, const qt_pauli* obs,
+                                  double* out, double* out_norm) {
+    if (!ctx || !state_dev || !out_norm || (n_obs > 0 && (!obs || !out))) return fail(QT_EINVAL, "bad argument");
+    qt_plan p = nullptr;
+    qt_status e = read_only_plan(n, &p);
+    if (e != QT_OK) return e;
+    const Plan& P = plan_of(p);
+    std::vector<ObsDesc> table;
+    ObsGroups og;
+    SingleExtras ex;
+    ex.out_norm = out_norm;
+    if ((e = parse_obs(n, P.T, P.CL, n_obs, obs, table, og)) == QT_OK)
+        e = run_single(ctx, p, const_cast<float2*>(reinterpret_cast<const float2*>(state_dev)), og, table, n_obs, 0,
+                       0, 0, nullptr, out, 1, nullptr, false, &ex);
     qt_plan_destroy(p);
     return e;
 }

@@ -93,6 +93,13 @@ def lib() -> ctypes.CDLL:
                                  ctypes.c_int),
         "qt_expectation_value": ([vp, vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(Pauli), dp], ctypes.c_int),
         "qt_kraus_lower_bound": ([ctypes.c_int, dp], ctypes.c_double),
+        "qt_add_matrix": ([vp, ctypes.c_int, ctypes.c_int, ip, dp], ctypes.c_int),
+        "qt_apply_plan": ([vp, vp, vp, ctypes.c_size_t], ctypes.c_int),
+        "qt_reduce_rho": ([vp, vp, ctypes.c_int, ctypes.c_int, ip, dp], ctypes.c_int),
+        "qt_sample_local": ([vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
+                             vp, vp], ctypes.c_int),
+        "qt_expectation_partials": ([vp, vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(Pauli), dp, dp],
+                                    ctypes.c_int),
         "qt_plan_info": ([vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
         "qt_last_error": ([], ctypes.c_char_p),
         "qt_version": ([], ctypes.c_char_p),
@@ -135,6 +142,12 @@ class Circuit:
         q = np.asarray(qubits, np.int32)
         m = _cplx(U)
         _check(lib().qt_add_gate(self.h, moment, len(q), _iptr(q), _dptr(m)))
+
+    def add_matrix(self, moment: int, qubits: Sequence[int], M) -> None:
+        """A general (e.g. non-unitary Kraus) operator; no unitarity check."""
+        q = np.asarray(qubits, np.int32)
+        m = _cplx(M)
+        _check(lib().qt_add_matrix(self.h, moment, len(q), _iptr(q), _dptr(m)))
 
     def add_channel(self, moment: int, qubits: Sequence[int], kraus: Iterable, record: bool = True) -> None:
         q = np.asarray(qubits, np.int32)
@@ -275,6 +288,37 @@ class Context:
         _check(lib().qt_sample_bitstrings(self.h, ctypes.c_void_p(state.data_ptr()), n, seed, traj, shots,
                                           out.ctypes.data))
         return out
+
+    # ---- distributed-state building blocks ------------------------------------
+    def apply_plan(self, plan: Plan, state) -> None:
+        _check(lib().qt_apply_plan(self.h, plan.h, ctypes.c_void_p(state.data_ptr()), state.numel() * 8))
+
+    def reduce_rho(self, state, qubits: Sequence[int]) -> np.ndarray:
+        """rho_Q in internal order (bit m <-> m-th lowest listed qubit), fp64."""
+        n = int(np.log2(state.numel()))
+        q = np.asarray(qubits, np.int32)
+        d = 1 << len(q)
+        out = np.zeros(2 * d * d, np.float64)
+        _check(lib().qt_reduce_rho(self.h, ctypes.c_void_p(state.data_ptr()), n, len(q), _iptr(q), _dptr(out)))
+        return out.view(np.complex128).reshape(d, d)
+
+    def sample_local(self, state, n_total: int, seed: int, traj: int, shot_ids: Sequence[int]) -> np.ndarray:
+        n = int(np.log2(state.numel()))
+        ids = np.ascontiguousarray(shot_ids, np.int32)
+        out = np.zeros(len(ids), np.uint64)
+        _check(lib().qt_sample_local(self.h, ctypes.c_void_p(state.data_ptr()), n, n_total, seed, traj, len(ids),
+                                     ids.ctypes.data if len(ids) else None, out.ctypes.data if len(ids) else None))
+        return out
+
+    def expectation_partials(self, state, observables: Sequence[str]):
+        n = int(np.log2(state.numel()))
+        out = np.zeros(max(len(observables), 1), np.float64)
+        norm = np.zeros(1, np.float64)
+        parr, keep = _pauli_array(observables)
+        _check(lib().qt_expectation_partials(self.h, ctypes.c_void_p(state.data_ptr()), n, len(observables), parr,
+                                             _dptr(out), _dptr(norm)))
+        del keep
+        return out[: len(observables)], float(norm[0])
 
     def expectation_value(self, state, observables: Sequence[str]) -> np.ndarray:
         n = int(np.log2(state.numel()))
