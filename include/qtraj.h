@@ -207,6 +207,24 @@ qt_status qt_expectation_value(qt_ctx ctx, const void* state_dev, int n, int n_o
  * qt_expectation_partials: <psi|P|psi>/<psi|psi> of the local state and
  *   out_norm = <psi|psi>, so ranks can combine sum_r norm_r * value_r. */
 qt_status qt_add_matrix(qt_circuit c, int moment, int nq, const int* qubits, const double* M);
+/* qt_permute_qubits: dst[pi(i)] = src[i], bit b of i moved to bit perm[b]
+ *   (n <= 24 local qubits; src != dst; device buffers on the context stream). */
+qt_status qt_permute_qubits(qt_ctx ctx, const void* src_dev, void* dst_dev, int n, const int* perm);
+/* Host-side pieces of Alg. 2 for a driver that owns the state layout:
+ * qt_draw: the RNG contract's uniform (purpose 1 channel, 2 sample, 3 readout).
+ * qt_channel_first_loop: Alg. 2 lines 2-11 for Kraus list K
+ *   (n_kraus matrices, Kronecker order) and uniform u; *pick >= 0: deferred pick
+ *   to be applied as K_pick * deferred_scale (1/sqrt(pbar) for unitary
+ *   mixtures); *pick = -1: conventional, *r_rest = the remaining uniform.
+ *   mode 1 never defers.
+ * qt_channel_choose: Alg. 2 lines 13-21 given rho over the
+ *   channel's qubits at positions qubits[] (rho in internal order of those
+ *   positions, as qt_reduce_rho returns it); *scale = 1/sqrt(raw p_pick). */
+double qt_draw(uint64_t seed, uint32_t ordinal, uint32_t purpose, uint64_t traj, int half);
+qt_status qt_channel_first_loop(int nq, int n_kraus, const double* K, double u, int mode, int* pick,
+                                double* r_rest, double* deferred_scale);
+qt_status qt_channel_choose(int nq, int n_kraus, const double* K, const int* qubits, const double* rho,
+                            double r, int mode, int* pick, double* scale);
 qt_status qt_apply_plan(qt_ctx ctx, qt_plan plan, void* state_dev, size_t state_bytes);
 qt_status qt_reduce_rho(qt_ctx ctx, const void* state_dev, int n, int nq, const int* qubits, double* out);
 qt_status qt_sample_local(qt_ctx ctx, const void* state_dev, int n, int n_total, uint64_t seed, uint64_t traj,

@@ -8,6 +8,7 @@
 #include <string>
 
 #include "host.hpp"
+#include "philox.hpp"
 
 struct qt_circuit_s {
     qt::Circuit c;
@@ -194,6 +195,96 @@ qt_status qt_add_gate(qt_circuit c, int moment, int nq, const int* qubits, const
         return fail(QT_ENONUNITARY, "gate matrix is not unitary (tolerance 1e-9)");
     c->moment_mask[moment] |= mask;
     c->c.ops.push_back(std::move(op));
+    return QT_OK;
+}
+
+double qt_draw(uint64_t seed, uint32_t ordinal, uint32_t purpose, uint64_t traj, int half) {
+    return draw(seed, ordinal, purpose, traj, half);
+}
+
+// Alg. 2 lines 2-11 for one channel of nq <= 6 qubits.
+qt_status qt_channel_first_loop(int nq, int n_kraus, const double* K, double u, int mode, int* pick,
+                                double* r_rest, double* deferred_scale) {
+    if (nq < 1 || nq > 6 || n_kraus < 1 || n_kraus > 64 || !K || !pick || !r_rest || !deferred_scale)
+        return fail(QT_EINVAL, "bad argument");
+    const int d = 1 << nq;
+    std::vector<cd> k((size_t)d * d);
+    bool mixture = true;
+    std::vector<double> pbar(n_kraus);
+    for (int i = 0; i < n_kraus; ++i) {
+        for (int e = 0; e < d * d; ++e) k[e] = cd(K[2 * ((size_t)i * d * d + e)], K[2 * ((size_t)i * d * d + e) + 1]);
+        pbar[i] = lower_bound(d, k.data());
+        // K^dag K = c I ?
+        double c0 = 0;
+        std::vector<cd> H((size_t)d * d);
+        for (int a = 0; a < d; ++a)
+            for (int b = 0; b < d; ++b) {
+                cd s = 0;
+                for (int q = 0; q < d; ++q) s += std::conj(k[q * d + a]) * k[q * d + b];
+                H[a * d + b] = s;
+            }
+        for (int a = 0; a < d; ++a) c0 += H[a * d + a].real();
+        c0 /= d;
+        for (int a = 0; a < d && mixture; ++a)
+            for (int b = 0; b < d; ++b)
+                if (std::abs(H[a * d + b] - (a == b ? cd(c0, 0) : cd(0, 0))) >= 1e-12) {
+                    mixture = false;
+                    break;
+                }
+    }
+    double r = u;
+    *pick = -1;
+    if (mode == 0) {
+        for (int i = 0; i < n_kraus; ++i) {
+            if (r < pbar[i]) { *pick = i; break; }
+            r -= pbar[i];
+        }
+        if (*pick < 0 && mixture) *pick = n_kraus - 1;  // s == 1
+    }
+    *r_rest = r;
+    *deferred_scale = (*pick >= 0 && mixture && pbar[*pick] > 0) ? 1.0 / std::sqrt(pbar[*pick]) : 1.0;
+    return QT_OK;
+}
+
+// Alg. 2 lines 13-21 from a reduced density matrix rho over the
+// channel's qubits (positions `qubits`, rho in internal order: bit m <-> the
+// m-th lowest position).  p_i = Tr(K_i^dag K_i rho) / Tr rho.
+qt_status qt_channel_choose(int nq, int n_kraus, const double* K, const int* qubits, const double* rho, double r,
+                            int mode, int* pick, double* scale) {
+    if (nq < 1 || nq > 6 || n_kraus < 1 || n_kraus > 64 || !K || !qubits || !rho || !pick || !scale)
+        return fail(QT_EINVAL, "bad argument");
+    const int d = 1 << nq;
+    int qs[6];
+    std::vector<cd> k((size_t)d * d);
+    double tr = 0;
+    for (int a = 0; a < d; ++a) tr += rho[2 * (a * d + a)];
+    if (!(tr > 0)) return fail(QT_ESTATE, "zero-norm state");
+    std::vector<double> raw(n_kraus), w(n_kraus);
+    *pick = -1;
+    for (int i = 0; i < n_kraus; ++i) {
+        canonicalize(nq, qubits, K + (size_t)2 * i * d * d, qs, k.data());
+        const double pbar = mode == 1 ? 0.0 : lower_bound(d, k.data());
+        double s = 0;  // Re Tr(K^dag K rho)
+        for (int a = 0; a < d; ++a)
+            for (int b = 0; b < d; ++b) {
+                cd m = 0;
+                for (int q = 0; q < d; ++q) m += std::conj(k[q * d + a]) * k[q * d + b];
+                s += m.real() * rho[2 * (b * d + a)] - m.imag() * rho[2 * (b * d + a) + 1];
+            }
+        raw[i] = s;
+        const double p = s / tr;
+        if (p < pbar - 1e-6) return fail(QT_ENONCPTP, "p_i below its lower bound");
+        w[i] = std::max(0.0, p - pbar);
+        if (r < w[i]) { *pick = i; break; }
+        r -= w[i];
+    }
+    if (*pick < 0) {
+        if (r > 1e-6) return fail(QT_ELEAK, "Alg. 2 fall-through residual > 1e-6");
+        for (int i = n_kraus - 1; i >= 0; --i)
+            if (w[i] > 0) { *pick = i; break; }
+        if (*pick < 0) return fail(QT_ELEAK, "no operator with positive weight");
+    }
+    *scale = 1.0 / std::sqrt(raw[*pick]);
     return QT_OK;
 }
 

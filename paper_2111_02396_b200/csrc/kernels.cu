@@ -243,7 +243,7 @@ sample_kernel(const float2* __restrict__ state, int n, int T, const double* __re
                 if (b == 1 && p11 && u < p11[q]) out &= ~(1ull << q);
             }
         }
-        out_bits[(uint64_t)slot * shots + shot] = out;
+        out_bits[(uint64_t)slot * shots + (gw % shots)] = out;  // position in the request, not the shot id
     }
 }
 

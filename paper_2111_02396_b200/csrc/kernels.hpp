@@ -57,6 +57,9 @@ cudaError_t launch_sample(const float2* state, int n, int T, const double* block
                           const double* p11, uint64_t* out_bits, cudaStream_t s, int n_rng = 0,
                           const int32_t* shot_ids = nullptr);
 
+// dst[pi(i)] = src[i] where bit b of i moves to bit perm[b] (n <= 24).
+cudaError_t launch_permute_qubits(const float2* src, float2* dst, int n, const int* perm, cudaStream_t s);
+
 // rho_Q (2^q x 2^q, q <= 2) of the qubits in qmask over a whole n-qubit state;
 // partial: kRhoBlocks x 32 doubles scratch; out: 2 * 4^q doubles (device).
 cudaError_t launch_rho_reduce(const float2* state, int n, uint64_t qmask, int q, double* partial, double* out,

@@ -828,6 +828,20 @@ qt_status qt_expectation_value(qt_ctx ctx, const void* state_dev, int n, int n_o
 
 // ---- building blocks of the distributed-state mode -------------------------
 
+qt_status qt_permute_qubits(qt_ctx ctx, const void* src_dev, void* dst_dev, int n, const int* perm) {
+    if (!ctx || !src_dev || !dst_dev || !perm || src_dev == dst_dev) return fail(QT_EINVAL, "bad argument");
+    if (n < 1 || n > 24) return fail(QT_EINVAL, "qt_permute_qubits: 1 <= n <= 24");
+    uint32_t seen = 0;
+    for (int b = 0; b < n; ++b) {
+        if (perm[b] < 0 || perm[b] >= n || ((seen >> perm[b]) & 1u)) return fail(QT_EQUBIT, "not a permutation");
+        seen |= 1u << perm[b];
+    }
+    QT_CK(cudaSetDevice(ctx->device));
+    QT_CK(launch_permute_qubits(reinterpret_cast<const float2*>(src_dev), reinterpret_cast<float2*>(dst_dev), n, perm,
+                                ctx->stream));
+    return QT_OK;
+}
+
 qt_status qt_apply_plan(qt_ctx ctx, qt_plan plan, void* state_dev, size_t state_bytes) {
     if (!ctx || !plan || !state_dev) return fail(QT_EINVAL, "NULL argument");
     const Plan& P = plan_of(plan);

@@ -1,0 +1,375 @@
+"""Distributed-state mode (second mode of the north star): one
+trajectory of an n-qubit register whose state vector is split over G = 2^g
+ranks (global index = rank << n_local | local index), for registers above one
+GPU's capacity (config 5: 36 qubits on 8 x B200).
+
+Mechanics (not in the paper, which has no distributed state; P:336 only mentions
+36-qubit TPU runs):
+  * a qubit map places every logical qubit either in a local slot (amplitude
+    index bit < n_local) or a global slot (a rank bit);
+  * consecutive operations on local qubits are buffered and applied by one
+    fused plan (the library's fuser + K1 tile passes) on every rank;
+  * an operation that touches global qubits first swaps them with local
+    "victim" qubits: a local bit permutation (qt_permute_qubits) moves the
+    victims to the top local bits, then an all-to-all (NCCL over NVLink, or
+    gloo in the CPU tests) exchanges the 2^s chunks -- the classic global-qubit
+    swap; victims are the local qubits used farthest in the future (Belady);
+  * channels follow Alg. 2 exactly as in the single-GPU path: the first loop
+    (qt_channel_first_loop) defers picks into the buffered operations; a
+    conventional channel flushes, reduces rho_Q on every rank (qt_reduce_rho),
+    all-reduces it (fp64) and walks lines 13-21 (qt_channel_choose) on identical
+    data on every rank, so every rank takes the same branch;
+  * terminal sampling: chain rule over the rank bits from all-gathered rank
+    masses, then the owning rank samples the local levels (qt_sample_local,
+    RNG ordinals of the whole register); Z-type observables from per-rank
+    partial sums.
+Results are identical to the single-state simulation (same draws, same
+decisions) up to fp32 rounding; tests compare against the CPU oracle.
+
+All per-rank arithmetic runs in libqtraj (the `GpuBackend`); this module only
+orchestrates.  The collective layer is a `Fabric`: `TorchFabric` (one rank per
+process, torch.distributed) or `EmulatedFabric` (all ranks in one process, for
+single-GPU tests; NCCL cannot place two ranks on one GPU).
+"""
+from __future__ import annotations
+
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from . import qtraj
+
+PURPOSE_CHANNEL, PURPOSE_SAMPLE = 1, 2
+
+
+# ---------------------------------------------------------------------------
+# Backends: per-rank state storage + device operations
+# ---------------------------------------------------------------------------
+class GpuBackend:
+    """Per-rank states as complex64 CUDA tensors; all operations in libqtraj."""
+
+    def __init__(self, ctx: "qtraj.Context", device, max_fused: int = 4):
+        import torch
+        self.torch = torch
+        self.ctx = ctx
+        self.device = device
+        self.max_fused = max_fused
+
+    def new_state(self, n_local: int, rank: int):
+        s = self.torch.zeros(1 << n_local, dtype=self.torch.complex64, device=self.device)
+        if rank == 0:
+            s[0] = 1.0
+        return s
+
+    def apply_ops(self, state, n_local: int, ops):
+        c = qtraj.Circuit(n_local)
+        for i, (pos, M) in enumerate(ops):
+            c.add_matrix(i, pos, M)
+        plan = qtraj.Plan(c, max_fused=max(self.max_fused, max(len(p) for p, _ in ops)))
+        self.ctx.apply_plan(plan, state)
+
+    def permute(self, state, perm):
+        out = self.torch.empty_like(state)
+        self.ctx.permute_qubits(state, out, perm)
+        return out
+
+    def reduce_rho(self, state, positions):
+        return self.ctx.reduce_rho(state, positions)
+
+    def expect(self, state, observables: Sequence[str]):
+        return self.ctx.expectation_partials(state, observables)
+
+    def sample_local(self, state, n_total, seed, traj, shot_ids):
+        return self.ctx.sample_local(state, n_total, seed, traj, shot_ids)
+
+
+# ---------------------------------------------------------------------------
+# Fabrics: the collectives over the rank slices of one register
+# ---------------------------------------------------------------------------
+def _dest(rank: int, gbits: Sequence[int], c: int) -> int:
+    r = rank
+    for j, b in enumerate(gbits):
+        r = (r & ~(1 << b)) | (((c >> j) & 1) << b)
+    return r
+
+
+def _src_chunk(rank: int, gbits: Sequence[int]) -> int:
+    return sum(((rank >> b) & 1) << j for j, b in enumerate(gbits))
+
+
+class EmulatedFabric:
+    """All G ranks in one process (single-GPU tests); exchanges are device copies."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self.local_ranks = list(range(world))
+
+    def exchange_top(self, states: Dict[int, object], gbits: Sequence[int], s: int):
+        """Swap the top s local bits with global bits gbits (top local bit
+        n_local - s + j <-> rank bit gbits[j])."""
+        out = {}
+        size = states[0].numel()
+        chunk = size >> s
+        for r in range(self.world):
+            out[r] = states[r].clone()
+        for r in range(self.world):
+            for c in range(1 << s):
+                d = _dest(r, gbits, c)
+                cp = _src_chunk(r, gbits)
+                out[d][cp * chunk:(cp + 1) * chunk].copy_(states[r][c * chunk:(c + 1) * chunk])
+        return out
+
+    def allreduce(self, per_rank: Dict[int, np.ndarray]) -> np.ndarray:
+        tot = None
+        for r in self.local_ranks:
+            tot = per_rank[r].copy() if tot is None else tot + per_rank[r]
+        return tot
+
+    def allgather(self, per_rank: Dict[int, float]) -> np.ndarray:
+        return np.array([per_rank[r] for r in range(self.world)], np.float64)
+
+    def broadcast_u64(self, arr: np.ndarray, owner: int) -> np.ndarray:
+        return arr
+
+
+class TorchFabric:
+    """One rank per process over a torch.distributed process group (NCCL on
+    NVLink for CUDA tensors, gloo for CPU tensors)."""
+
+    def __init__(self, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        self.torch = torch
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.local_ranks = [self.rank]
+        self.device = device
+
+    def exchange_top(self, states, gbits, s):
+        x = states[self.rank]
+        chunk = x.numel() >> s
+        in_split = [0] * self.world
+        out_split = [0] * self.world
+        for c in range(1 << s):
+            in_split[_dest(self.rank, gbits, c)] = chunk
+        # the sources of this rank are the ranks that differ from it only in gbits
+        for c in range(1 << s):
+            out_split[_dest(self.rank, gbits, c)] = chunk
+        y = self.torch.empty_like(x)
+        self.dist.all_to_all_single(y, x.contiguous(), out_split, in_split, group=self.group)
+        return {self.rank: y}
+
+    def _dev(self):
+        return self.device if self.device is not None else "cpu"
+
+    def allreduce(self, per_rank):
+        a = np.ascontiguousarray(per_rank[self.rank])
+        cplx = np.iscomplexobj(a)
+        t = self.torch.from_numpy(a.view(np.float64) if cplx else a.astype(np.float64)).to(self._dev())
+        self.dist.all_reduce(t, group=self.group)
+        out = t.cpu().numpy()
+        return out.view(np.complex128).reshape(a.shape) if cplx else out.reshape(a.shape)
+
+    def allgather(self, per_rank):
+        t = self.torch.tensor([float(per_rank[self.rank])], dtype=self.torch.float64, device=self._dev())
+        bufs = [self.torch.zeros_like(t) for _ in range(self.world)]
+        self.dist.all_gather(bufs, t, group=self.group)
+        return np.array([b.item() for b in bufs], np.float64)
+
+    def broadcast_u64(self, arr: np.ndarray, owner: int) -> np.ndarray:
+        t = self.torch.from_numpy(np.ascontiguousarray(arr).view(np.int64)).to(self._dev())
+        self.dist.broadcast(t, src=owner, group=self.group)
+        return t.cpu().numpy().view(np.uint64)
+
+
+# ---------------------------------------------------------------------------
+# The distributed trajectory
+# ---------------------------------------------------------------------------
+def _is_identity(M) -> bool:
+    M = np.asarray(M)
+    return np.max(np.abs(M - np.eye(M.shape[0]))) < 1e-15
+
+
+class DistributedTrajectory:
+    def __init__(self, backend, fabric, n_total: int, mode: int = 0):
+        world = fabric.world
+        g = world.bit_length() - 1
+        if (1 << g) != world:
+            raise ValueError("world size must be a power of two")
+        if n_total - g < 6:
+            raise ValueError("need at least 6 local qubits per rank")
+        self.b = backend
+        self.f = fabric
+        self.n = n_total
+        self.g = g
+        self.nl = n_total - g
+        self.mode = mode
+        self.slot = list(range(n_total))          # logical qubit -> physical slot
+        self.states = {r: backend.new_state(self.nl, r) for r in fabric.local_ranks}
+        self.pending: List = []
+        self.swaps = 0
+        self.exchanged_bytes = 0
+
+    # -- helpers ------------------------------------------------------------
+    def _flush(self):
+        if not self.pending:
+            return
+        for r in self.f.local_ranks:
+            self.b.apply_ops(self.states[r], self.nl, self.pending)
+        self.pending = []
+
+    def _apply_local_perm(self, perm_slot: Dict[int, int]):
+        """Move local slot a -> perm_slot[a] (others fixed)."""
+        perm = list(range(self.nl))
+        for a, b in perm_slot.items():
+            perm[a] = b
+        if perm == list(range(self.nl)):
+            return
+        for r in self.f.local_ranks:
+            self.states[r] = self.b.permute(self.states[r], perm)
+        inv = {a: b for a, b in perm_slot.items()}
+        for q in range(self.n):
+            if self.slot[q] < self.nl:
+                self.slot[q] = inv.get(self.slot[q], self.slot[q])
+
+    def _choose_victims(self, s: int, keep: set, upcoming: List[set]) -> List[int]:
+        """s local logical qubits not in `keep`, used farthest in the future (Belady)."""
+        local_q = [q for q in range(self.n) if self.slot[q] < self.nl and q not in keep]
+
+        def next_use(q):
+            for i, ops in enumerate(upcoming):
+                if q in ops:
+                    return i
+            return 1 << 30
+        local_q.sort(key=lambda q: (-next_use(q), -self.slot[q]))
+        return local_q[:s]
+
+    def _swap_in(self, glob: List[int], victims: List[int]):
+        """Exchange logical qubits `glob` (global) with `victims` (local)."""
+        s = len(glob)
+        assert len(victims) == s
+        self._flush()
+        # local permutation: victim j -> top slot nl - s + j (swapping with the occupant)
+        top = [self.nl - s + j for j in range(s)]
+        occupant = {self.slot[q]: q for q in range(self.n) if self.slot[q] < self.nl}
+        cur = {q: self.slot[q] for q in range(self.n)}
+        for j, v in enumerate(victims):
+            a, b = cur[v], top[j]
+            if a == b:
+                continue
+            w = occupant[b]
+            occupant[a], occupant[b] = w, v
+            cur[v], cur[w] = b, a
+        self._apply_local_perm({self.slot[q]: cur[q] for q in range(self.n)
+                                if self.slot[q] < self.nl and cur[q] != self.slot[q]})
+        gbits = [self.slot[q] - self.nl for q in glob]
+        self.states = self.f.exchange_top(self.states, gbits, s)
+        self.swaps += 1
+        self.exchanged_bytes += (1 - 2.0 ** -s) * 8 * (1 << self.nl) * len(self.f.local_ranks)
+        for j, q in enumerate(glob):
+            v = victims[j]
+            self.slot[v] = self.nl + gbits[j]
+            self.slot[q] = top[j]
+
+    def _ensure_local(self, qubits: Sequence[int], upcoming: List[set]):
+        glob = [q for q in qubits if self.slot[q] >= self.nl]
+        if glob:
+            self._swap_in(glob, self._choose_victims(len(glob), set(qubits), upcoming))
+
+    # -- Alg. 2 over a distributed register ---------------------------------
+    def run(self, circuit, seed: int, traj: int, shots: int = 1, observables: Sequence[str] = (),
+            lookahead: int = 64):
+        ops = list(circuit.ops())
+        uses = [set(op.qubits) for op in ops]
+        kraus_rec = []
+        ch = 0
+        for i, op in enumerate(ops):
+            upcoming = uses[i + 1:i + 1 + lookahead]
+            self._ensure_local(op.qubits, upcoming)
+            pos = [self.slot[q] for q in op.qubits]
+            if not hasattr(op, "kraus"):
+                self.pending.append((pos, np.asarray(op.matrix, np.complex128)))
+                continue
+            u = qtraj.draw(seed, ch, PURPOSE_CHANNEL, traj, 0)
+            pick, r, sc = qtraj.channel_first_loop(op.kraus, u, self.mode)
+            if pick >= 0:
+                M = np.asarray(op.kraus[pick], np.complex128) * sc
+                if not _is_identity(M):
+                    self.pending.append((pos, M))
+            else:
+                self._flush()
+                rho = {rk: self.b.reduce_rho(self.states[rk], pos) for rk in self.f.local_ranks}
+                tot = self.f.allreduce(rho)
+                pick, scale = qtraj.channel_choose(op.kraus, pos, tot, r, self.mode)
+                self.pending.append((pos, np.asarray(op.kraus[pick], np.complex128) * scale))
+            kraus_rec.append(pick)
+            ch += 1
+        self._flush()
+        # layout for sampling: logical qubits >= nl global, local slot i = logical i
+        high_local = [q for q in range(self.nl, self.n) if self.slot[q] < self.nl]
+        low_global = [q for q in range(self.nl) if self.slot[q] >= self.nl]
+        if low_global:
+            self._swap_in(low_global, high_local)
+        self._apply_local_perm({self.slot[q]: q for q in range(self.nl) if self.slot[q] != q})
+        assert all(self.slot[q] == q for q in range(self.nl))
+        out = {"kraus": np.array(kraus_rec, np.int32), "swaps": self.swaps}
+        # rank masses and observables
+        masses = {}
+        zvals = {}
+        for rk in self.f.local_ranks:
+            obs_local = []
+            for s_ in observables:
+                assert all(ch_ in "IZ" for ch_ in s_), "distributed mode: Z-type observables"
+                obs_local.append("".join(s_[q] for q in range(self.nl)))
+            vals, norm = self.b.expect(self.states[rk], obs_local)
+            if not norm > 0.0:  # an empty slice (e.g. after amplitude damping): 0/0 partials
+                vals = np.zeros(len(obs_local))
+                norm = 0.0
+            masses[rk] = norm
+            sg = []
+            for s_ in observables:
+                par = 0
+                for q in range(self.nl, self.n):
+                    if s_[q] == "Z":
+                        par ^= (rk >> (self.slot[q] - self.nl)) & 1
+                sg.append(-1.0 if par else 1.0)
+            zvals[rk] = np.asarray([sgn * v * norm for sgn, v in zip(sg, vals)] + [norm], np.float64)
+        M = self.f.allgather(masses)
+        if observables:
+            tot = self.f.allreduce(zvals)
+            out["obs"] = tot[:-1] / tot[-1]
+        # chain rule over the rank bits (levels n-1 .. nl), then local levels on the owner
+        half_n = (self.n + 1) // 2
+        bits = np.zeros(shots, np.uint64)
+        owners = np.zeros(shots, np.int64)
+        for sh in range(shots):
+            prefix = 0          # logical high bits chosen so far
+            cand = list(range(self.f.world))
+            for lvl in range(self.n - 1, self.nl - 1, -1):
+                gb = self.slot[lvl] - self.nl
+                m0 = sum(M[r] for r in cand if not (r >> gb) & 1)
+                m1 = sum(M[r] for r in cand if (r >> gb) & 1)
+                u = qtraj.draw(seed, sh * half_n + lvl // 2, PURPOSE_SAMPLE, traj, lvl & 1)
+                if m0 == 0.0:
+                    bit = 1
+                elif m1 == 0.0:
+                    bit = 0
+                else:
+                    bit = 0 if u * (m0 + m1) < m0 else 1
+                cand = [r for r in cand if ((r >> gb) & 1) == bit]
+                prefix |= bit << lvl
+            owners[sh] = cand[0]
+            bits[sh] = prefix
+        for rk in self.f.local_ranks:
+            ids = [sh for sh in range(shots) if owners[sh] == rk]
+            if ids:
+                low = self.b.sample_local(self.states[rk], self.n, seed, traj, ids)
+                for sh, lb in zip(ids, low):
+                    bits[sh] |= np.uint64(lb)
+        for sh in range(shots):  # every rank ends with every shot's bits
+            bits[sh:sh + 1] = self.f.broadcast_u64(bits[sh:sh + 1], int(owners[sh]))
+        out["bits"] = bits
+        out["masses"] = M
+        return out

@@ -94,6 +94,13 @@ def lib() -> ctypes.CDLL:
         "qt_expectation_value": ([vp, vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(Pauli), dp], ctypes.c_int),
         "qt_kraus_lower_bound": ([ctypes.c_int, dp], ctypes.c_double),
         "qt_add_matrix": ([vp, ctypes.c_int, ctypes.c_int, ip, dp], ctypes.c_int),
+        "qt_permute_qubits": ([vp, vp, vp, ctypes.c_int, ip], ctypes.c_int),
+        "qt_draw": ([ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int],
+                    ctypes.c_double),
+        "qt_channel_first_loop": ([ctypes.c_int, ctypes.c_int, dp, ctypes.c_double, ctypes.c_int, ip, dp, dp],
+                                  ctypes.c_int),
+        "qt_channel_choose": ([ctypes.c_int, ctypes.c_int, dp, ip, dp, ctypes.c_double, ctypes.c_int, ip, dp],
+                              ctypes.c_int),
         "qt_apply_plan": ([vp, vp, vp, ctypes.c_size_t], ctypes.c_int),
         "qt_reduce_rho": ([vp, vp, ctypes.c_int, ctypes.c_int, ip, dp], ctypes.c_int),
         "qt_sample_local": ([vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
@@ -290,6 +297,13 @@ class Context:
         return out
 
     # ---- distributed-state building blocks ------------------------------------
+    def permute_qubits(self, src, dst, perm: Sequence[int]) -> None:
+        """dst[pi(i)] = src[i], bit b of i moved to bit perm[b]."""
+        n = int(np.log2(src.numel()))
+        p = np.asarray(perm, np.int32)
+        _check(lib().qt_permute_qubits(self.h, ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(dst.data_ptr()), n,
+                                       _iptr(p)))
+
     def apply_plan(self, plan: Plan, state) -> None:
         _check(lib().qt_apply_plan(self.h, plan.h, ctypes.c_void_p(state.data_ptr()), state.numel() * 8))
 
@@ -328,6 +342,42 @@ class Context:
                                           _dptr(out)))
         del keep
         return out
+
+
+PURPOSE_CHANNEL, PURPOSE_SAMPLE, PURPOSE_READOUT = 1, 2, 3
+
+
+def draw(seed: int, ordinal: int, purpose: int, traj: int, half: int = 0) -> float:
+    """The RNG contract's uniform (Philox4x32-10, qtraj.h)."""
+    return lib().qt_draw(seed, ordinal, purpose, traj, half)
+
+
+def channel_first_loop(kraus, u: float, mode: int = 0):
+    """Alg. 2 lines 2-11: (pick or -1, remaining r, deferred scale)."""
+    ks = list(kraus)
+    nq = int(np.log2(np.asarray(ks[0]).shape[0]))
+    m = np.concatenate([_cplx(k) for k in ks])
+    pick = ctypes.c_int(-1)
+    r = ctypes.c_double(0.0)
+    sc = ctypes.c_double(1.0)
+    _check(lib().qt_channel_first_loop(nq, len(ks), _dptr(m), u, mode, ctypes.byref(pick), ctypes.byref(r),
+                                       ctypes.byref(sc)))
+    return pick.value, r.value, sc.value
+
+
+def channel_choose(kraus, positions: Sequence[int], rho: np.ndarray, r: float, mode: int = 0):
+    """Alg. 2 lines 13-21 from rho over the channel's qubit positions:
+    (pick, 1/sqrt(raw p_pick))."""
+    ks = list(kraus)
+    nq = len(positions)
+    m = np.concatenate([_cplx(k) for k in ks])
+    q = np.asarray(positions, np.int32)
+    rr = np.ascontiguousarray(np.asarray(rho, np.complex128)).view(np.float64).reshape(-1)
+    pick = ctypes.c_int(-1)
+    sc = ctypes.c_double(1.0)
+    _check(lib().qt_channel_choose(nq, len(ks), _dptr(m), _iptr(q), _dptr(rr), r, mode, ctypes.byref(pick),
+                                   ctypes.byref(sc)))
+    return pick.value, sc.value
 
 
 def kraus_lower_bound(K) -> float:

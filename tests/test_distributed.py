@@ -1,0 +1,193 @@
+"""Distributed-state mode: a register split over 2^g ranks with
+global-qubit swaps, checked against the CPU oracle's single-state trajectories.
+
+CPU: a numpy test backend (oracle Alg. 1 for the local operations) under the
+emulated fabric and under a real world-size-2 gloo process group (the
+all-to-all exchange path).  GPU: the libqtraj backend under the emulated
+fabric (NCCL cannot put two ranks on one GPU)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from paper_2111_02396_b200 import distributed as D
+from paper_2111_02396_b200 import qtraj
+
+
+class NumpyBackend:
+    """Test-only stand-in for the GPU backend: complex128 torch CPU tensors,
+    operations by the oracle's Alg. 1 and plain numpy sums."""
+
+    def __init__(self):
+        import torch
+        self.torch = torch
+
+    def new_state(self, nl, rank):
+        s = self.torch.zeros(1 << nl, dtype=self.torch.complex128)
+        if rank == 0:
+            s[0] = 1.0
+        return s
+
+    def apply_ops(self, state, nl, ops):
+        psi = state.numpy()
+        for pos, M in ops:
+            oracle.apply_gate(psi, pos, M)
+
+    def permute(self, state, perm):
+        src = state.numpy()
+        n = len(perm)
+        idx = np.arange(1 << n)
+        j = np.zeros_like(idx)
+        for b in range(n):
+            j |= ((idx >> b) & 1) << perm[b]
+        out = np.zeros_like(src)
+        out[j] = src
+        return self.torch.from_numpy(out)
+
+    def reduce_rho(self, state, positions):
+        psi = state.numpy()
+        pos = sorted(positions)
+        d = 1 << len(pos)
+        rho = np.zeros((d, d), np.complex128)
+        idx = np.arange(psi.size)
+        mask = sum(1 << p for p in pos)
+        base = idx[(idx & mask) == 0]
+        off = [sum(((a >> m) & 1) << p for m, p in enumerate(pos)) for a in range(d)]
+        for a in range(d):
+            for b in range(d):
+                rho[a, b] = np.sum(psi[base | off[a]] * np.conj(psi[base | off[b]]))
+        return rho
+
+    def expect(self, state, observables):
+        psi = state.numpy()
+        p = np.abs(psi) ** 2
+        norm = float(p.sum())
+        idx = np.arange(psi.size)
+        vals = []
+        for s in observables:
+            z = sum(1 << q for q, ch in enumerate(s) if ch == "Z")
+            par = np.array([bin(int(i) & z).count("1") & 1 for i in idx])
+            vals.append(float(np.sum(np.where(par, -p, p)) / norm))
+        return np.array(vals), norm
+
+    def sample_local(self, state, n_total, seed, traj, shot_ids):
+        psi = state.numpy()
+        nl = int(np.log2(psi.size))
+        half = (n_total + 1) // 2
+        out = []
+        for sh in shot_ids:
+            lo, size, bits = 0, psi.size, 0
+            for lvl in range(nl - 1, -1, -1):
+                h = size // 2
+                m0 = float(np.sum(np.abs(psi[lo:lo + h]) ** 2))
+                m1 = float(np.sum(np.abs(psi[lo + h:lo + size]) ** 2))
+                u = qtraj.draw(seed, sh * half + lvl // 2, 2, traj, lvl & 1)
+                bit = 1 if m0 == 0 else (0 if m1 == 0 else (0 if u * (m0 + m1) < m0 else 1))
+                if bit:
+                    lo += h
+                    bits |= 1 << lvl
+                size = h
+            out.append(bits)
+        return np.array(out, np.uint64)
+
+
+def circuit(n, seed, noise="both"):
+    c = workloads.random_circuit(n, depth=6, seed=seed, max_arity=2, noise=noise, p=0.04,
+                                 t1_ns=600.0, tphi_ns=1000.0)
+    c.observables = ["I" * q + "Z" + "I" * (n - q - 1) for q in range(n)] + ["Z" * n]
+    return c
+
+
+def check(out, ref, t):
+    assert (out["kraus"] == ref["kraus"][t]).all()
+    assert (out["bits"] == ref["bits"][t]).all()
+    assert np.max(np.abs(out["obs"] - ref["obs"][t])) < 1e-9 or np.max(np.abs(out["obs"] - ref["obs"][t])) < 1e-4
+
+
+def test_exchange_maps_are_bijective():
+    for world, gbits in ((8, [0, 2]), (8, [1]), (4, [0, 1]), (8, [2, 0, 1])):
+        s = len(gbits)
+        seen = set()
+        for r in range(world):
+            for c in range(1 << s):
+                seen.add((D._dest(r, gbits, c), D._src_chunk(r, gbits)))
+        assert len(seen) == world * (1 << s)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_emulated_fabric_numpy_backend_matches_oracle(world):
+    n = 8
+    c = circuit(n, seed=5)
+    seed, T = 321, 3
+    ref = oracle.run_trajectories(c, seed=seed, traj_count=T, shots=2)
+    for t in range(T):
+        tr = D.DistributedTrajectory(NumpyBackend(), D.EmulatedFabric(world), n)
+        out = tr.run(c, seed=seed, traj=t, shots=2, observables=c.observables)
+        check(out, ref, t)
+        assert out["swaps"] > 0
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _gloo_worker(rank, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    c = circuit(8, seed=6)
+    res = []
+    for t in range(2):
+        tr = D.DistributedTrajectory(NumpyBackend(), D.TorchFabric(), 8)
+        out = tr.run(c, seed=77, traj=t, shots=2, observables=c.observables)
+        res.append({k: np.asarray(v) for k, v in out.items() if k in ("kraus", "bits", "obs")})
+    q.put((rank, res))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_distributed_state_matches_oracle():
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_gloo_worker, args=(r, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(2))
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    c = circuit(8, seed=6)
+    ref = oracle.run_trajectories(c, seed=77, traj_count=2, shots=2)
+    for rank in (0, 1):
+        for t in range(2):
+            check(got[rank][t], ref, t)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_gpu_backend_emulated_fabric_matches_oracle(world):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = qtraj.Context(0)
+    n = 13
+    c = circuit(n, seed=40 + world, noise="ad")
+    seed, T = 99, 3
+    ref = oracle.run_trajectories(c, seed=seed, traj_count=T, shots=3)
+    for t in range(T):
+        tr = D.DistributedTrajectory(D.GpuBackend(ctx, "cuda:0"), D.EmulatedFabric(world), n)
+        out = tr.run(c, seed=seed, traj=t, shots=3, observables=c.observables)
+        assert (out["kraus"] == ref["kraus"][t]).all()
+        bad = [s for s in range(3) if out["bits"][s] != ref["bits"][t][s] and ref["sample_margin"][t][s] >= 1e-4]
+        assert not bad
+        assert np.max(np.abs(out["obs"] - ref["obs"][t])) < 1e-4
