@@ -208,7 +208,7 @@ qt_status qt_expectation_value(qt_ctx ctx, const void* state_dev, int n, int n_o
  *   out_norm = <psi|psi>, so ranks can combine sum_r norm_r * value_r. */
 qt_status qt_add_matrix(qt_circuit c, int moment, int nq, const int* qubits, const double* M);
 /* qt_permute_qubits: dst[pi(i)] = src[i], bit b of i moved to bit perm[b]
- *   (n <= 24 local qubits; src != dst; device buffers on the context stream). */
+ *   (n <= 40 local qubits; src != dst; device buffers on the context stream). */
 qt_status qt_permute_qubits(qt_ctx ctx, const void* src_dev, void* dst_dev, int n, const int* perm);
 /* Host-side pieces of Alg. 2 for a driver that owns the state layout:
  * qt_draw: the RNG contract's uniform (purpose 1 channel, 2 sample, 3 readout).

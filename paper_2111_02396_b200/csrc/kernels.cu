@@ -317,29 +317,41 @@ __global__ void rho_final_kernel(const double* __restrict__ partial, int ne, dou
 
 // Qubit permutation copy: dst[pi(i)] = src[i], bit j of i moves to bit perm[j]
 // (distributed-state mode: gathers the swapped local qubits into the top bits).
+struct QubitPerm {
+    uint8_t p[48];  // destination bit of source bit b
+};
+
+// Bits that stay in place are copied with one mask; only moved bits are
+// visited, so a swap of the top local bits costs a few operations per element
+// and keeps the low bits (coalescing) intact.
 __global__ void __launch_bounds__(256)
-permute_qubits_kernel(const float2* __restrict__ src, float2* __restrict__ dst, int n, const uint32_t perm_lo,
-                      const uint32_t perm_hi, const uint32_t perm_hh, const uint32_t perm_x) {
-    // perm packed 5 bits per qubit (n <= 34): words lo (q 0..5), hi (6..11), hh (12..17), x (18..23)
+permute_qubits_kernel(const float2* __restrict__ src, float2* __restrict__ dst, int n, uint64_t fixed_mask,
+                      int n_moved, const QubitPerm moved_src, const QubitPerm moved_dst) {
     const uint64_t total = 1ull << n;
     for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < total; i += (uint64_t)gridDim.x * 256) {
-        uint64_t j = 0;
-        for (int b = 0; b < n; ++b) {
-            const uint32_t w = b < 6 ? perm_lo : (b < 12 ? perm_hi : (b < 18 ? perm_hh : perm_x));
-            const int p = (int)((w >> (5 * (b % 6))) & 31u);
-            j |= ((i >> b) & 1ull) << p;
-        }
+        uint64_t j = i & fixed_mask;
+        for (int k = 0; k < n_moved; ++k) j |= ((i >> moved_src.p[k]) & 1ull) << moved_dst.p[k];
         dst[j] = src[i];
     }
 }
 
 cudaError_t launch_permute_qubits(const float2* src, float2* dst, int n, const int* perm, cudaStream_t s) {
-    if (n > 24) return cudaErrorInvalidValue;
-    uint32_t w[4] = {0, 0, 0, 0};
-    for (int b = 0; b < n; ++b) w[b / 6] |= (uint32_t)perm[b] << (5 * (b % 6));
+    if (n > 48) return cudaErrorInvalidValue;
+    QubitPerm ms{}, md{};
+    uint64_t fixed = 0;
+    int nm = 0;
+    for (int b = 0; b < n; ++b) {
+        if (perm[b] == b) {
+            fixed |= 1ull << b;
+        } else {
+            ms.p[nm] = (uint8_t)b;
+            md.p[nm] = (uint8_t)perm[b];
+            ++nm;
+        }
+    }
     const uint64_t total = 1ull << n;
-    const unsigned blocks = (unsigned)std::min<uint64_t>((total + 255) / 256, 148 * 16);
-    permute_qubits_kernel<<<blocks, 256, 0, s>>>(src, dst, n, w[0], w[1], w[2], w[3]);
+    const unsigned blocks = (unsigned)std::min<uint64_t>((total + 255) / 256, 148 * 32);
+    permute_qubits_kernel<<<blocks, 256, 0, s>>>(src, dst, n, fixed, nm, ms, md);
     return cudaGetLastError();
 }
 

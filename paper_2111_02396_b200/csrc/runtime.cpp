@@ -830,11 +830,11 @@ qt_status qt_expectation_value(qt_ctx ctx, const void* state_dev, int n, int n_o
 
 qt_status qt_permute_qubits(qt_ctx ctx, const void* src_dev, void* dst_dev, int n, const int* perm) {
     if (!ctx || !src_dev || !dst_dev || !perm || src_dev == dst_dev) return fail(QT_EINVAL, "bad argument");
-    if (n < 1 || n > 24) return fail(QT_EINVAL, "qt_permute_qubits: 1 <= n <= 24");
-    uint32_t seen = 0;
+    if (n < 1 || n > 40) return fail(QT_EINVAL, "qt_permute_qubits: 1 <= n <= 40");
+    uint64_t seen = 0;
     for (int b = 0; b < n; ++b) {
-        if (perm[b] < 0 || perm[b] >= n || ((seen >> perm[b]) & 1u)) return fail(QT_EQUBIT, "not a permutation");
-        seen |= 1u << perm[b];
+        if (perm[b] < 0 || perm[b] >= n || ((seen >> perm[b]) & 1ull)) return fail(QT_EQUBIT, "not a permutation");
+        seen |= 1ull << perm[b];
     }
     QT_CK(cudaSetDevice(ctx->device));
     QT_CK(launch_permute_qubits(reinterpret_cast<const float2*>(src_dev), reinterpret_cast<float2*>(dst_dev), n, perm,

@@ -69,9 +69,23 @@ class GpuBackend:
         self.ctx.apply_plan(plan, state)
 
     def permute(self, state, perm):
-        out = self.torch.empty_like(state)
+        # ping-pong with one spare buffer per size: a 33-qubit slice (64 GiB)
+        # and its spare fit in one B200's 180 GB
+        spare = getattr(self, "_spare", None)
+        out = spare if (spare is not None and spare.numel() == state.numel()) else self.torch.empty_like(state)
         self.ctx.permute_qubits(state, out, perm)
+        self._spare = state
         return out
+
+    def take_spare(self, like):
+        spare = getattr(self, "_spare", None)
+        if spare is not None and spare.numel() == like.numel():
+            self._spare = None
+            return spare
+        return self.torch.empty_like(like)
+
+    def give_spare(self, t):
+        self._spare = t
 
     def reduce_rho(self, state, positions):
         return self.ctx.reduce_rho(state, positions)
@@ -104,7 +118,7 @@ class EmulatedFabric:
         self.world = world
         self.local_ranks = list(range(world))
 
-    def exchange_top(self, states: Dict[int, object], gbits: Sequence[int], s: int):
+    def exchange_top(self, states: Dict[int, object], gbits: Sequence[int], s: int, pool=None):
         """Swap the top s local bits with global bits gbits (top local bit
         n_local - s + j <-> rank bit gbits[j])."""
         out = {}
@@ -147,7 +161,7 @@ class TorchFabric:
         self.local_ranks = [self.rank]
         self.device = device
 
-    def exchange_top(self, states, gbits, s):
+    def exchange_top(self, states, gbits, s, pool=None):
         x = states[self.rank]
         chunk = x.numel() >> s
         in_split = [0] * self.world
@@ -157,8 +171,11 @@ class TorchFabric:
         # the sources of this rank are the ranks that differ from it only in gbits
         for c in range(1 << s):
             out_split[_dest(self.rank, gbits, c)] = chunk
-        y = self.torch.empty_like(x)
+        # receive into the backend's spare buffer; the sent buffer becomes the spare
+        y = pool.take_spare(x) if hasattr(pool, "take_spare") else self.torch.empty_like(x)
         self.dist.all_to_all_single(y, x.contiguous(), out_split, in_split, group=self.group)
+        if hasattr(pool, "give_spare"):
+            pool.give_spare(x)
         return {self.rank: y}
 
     def _dev(self):
@@ -192,6 +209,11 @@ def _is_identity(M) -> bool:
     return np.max(np.abs(M - np.eye(M.shape[0]))) < 1e-15
 
 
+def _is_diag(M) -> bool:
+    M = np.asarray(M)
+    return not np.any(M - np.diag(np.diag(M)))
+
+
 class DistributedTrajectory:
     def __init__(self, backend, fabric, n_total: int, mode: int = 0):
         world = fabric.world
@@ -208,17 +230,56 @@ class DistributedTrajectory:
         self.mode = mode
         self.slot = list(range(n_total))          # logical qubit -> physical slot
         self.states = {r: backend.new_state(self.nl, r) for r in fabric.local_ranks}
-        self.pending: List = []
+        self.pending: List = []        # shared local operations (since the last flush)
+        self.pending_all: List = []    # (rank or -1 = every rank, positions, matrix), program order
+        self.rank_ops = {r: [] for r in fabric.local_ranks}
         self.swaps = 0
         self.exchanged_bytes = 0
 
     # -- helpers ------------------------------------------------------------
     def _flush(self):
-        if not self.pending:
+        if not self.pending and not any(self.rank_ops.values()):
             return
         for r in self.f.local_ranks:
-            self.b.apply_ops(self.states[r], self.nl, self.pending)
+            # shared ops and this rank's diagonal restrictions, in program order
+            ops = [o for o in self.pending_all if o[0] == -1 or o[0] == r]
+            if ops:
+                self.b.apply_ops(self.states[r], self.nl, [(p, M) for _, p, M in ops])
         self.pending = []
+        self.pending_all = []
+        self.rank_ops = {r: [] for r in self.f.local_ranks}
+
+    def _push(self, pos, M):
+        self.pending.append((pos, M))
+        self.pending_all.append((-1, pos, M))
+
+    def _push_diag_global(self, qubits, M):
+        """A diagonal operator touching global qubits, applied without a swap:
+        on rank r it is the diagonal restricted to r's values of the global
+        qubits, i.e. an operator on the local qubits only (or a scalar)."""
+        M = np.asarray(M, np.complex128)
+        nq = len(qubits)
+        d = np.diag(M)
+        loc = [m for m, q in enumerate(qubits) if self.slot[q] < self.nl]
+        for r in self.f.local_ranks:
+            gval = {m: (r >> (self.slot[q] - self.nl)) & 1 for m, q in enumerate(qubits) if self.slot[q] >= self.nl}
+            k = len(loc)
+            dd = np.zeros(1 << k, np.complex128)
+            for a in range(1 << k):
+                idx = 0
+                for m in range(nq):
+                    if m in gval:
+                        bit = gval[m]
+                    else:
+                        bit = (a >> (k - 1 - loc.index(m))) & 1
+                    idx |= bit << (nq - 1 - m)
+                dd[a] = d[idx]
+            if k == 0:  # a scalar on this rank
+                if dd[0] != 1.0:
+                    self.pending_all.append((r, [0], np.diag([dd[0], dd[0]])))
+            elif not np.all(dd == 1.0):
+                self.pending_all.append((r, [self.slot[qubits[m]] for m in loc], np.diag(dd)))
+            self.rank_ops[r].append(1)
 
     def _apply_local_perm(self, perm_slot: Dict[int, int]):
         """Move local slot a -> perm_slot[a] (others fixed)."""
@@ -265,13 +326,42 @@ class DistributedTrajectory:
         self._apply_local_perm({self.slot[q]: cur[q] for q in range(self.n)
                                 if self.slot[q] < self.nl and cur[q] != self.slot[q]})
         gbits = [self.slot[q] - self.nl for q in glob]
-        self.states = self.f.exchange_top(self.states, gbits, s)
+        self.states = self.f.exchange_top(self.states, gbits, s, pool=self.b)
         self.swaps += 1
         self.exchanged_bytes += (1 - 2.0 ** -s) * 8 * (1 << self.nl) * len(self.f.local_ranks)
         for j, q in enumerate(glob):
             v = victims[j]
             self.slot[v] = self.nl + gbits[j]
             self.slot[q] = top[j]
+
+    def _rho_diag_global(self, qubits: Sequence[int]):
+        """Diagonal of rho_Q over qubits some of which are global: rank r holds
+        the entries whose global bits equal r's.  Returns per-rank matrices in
+        the internal order of the sorted slot positions, and those positions."""
+        pos = [self.slot[q] for q in qubits]
+        order = sorted(pos)
+        d = 1 << len(pos)
+        loc = [p for p in order if p < self.nl]
+        out = {}
+        for rk in self.f.local_ranks:
+            rho = np.zeros((d, d), np.complex128)
+            if loc:
+                rl = self.b.reduce_rho(self.states[rk], loc)
+                diag_l = np.real(np.diag(rl))
+            else:
+                _, norm = self.b.expect(self.states[rk], [])
+                diag_l = np.array([norm])
+            for a_l in range(1 << len(loc)):
+                a = 0
+                for m, p in enumerate(order):
+                    if p < self.nl:
+                        bit = (a_l >> loc.index(p)) & 1
+                    else:
+                        bit = (rk >> (p - self.nl)) & 1
+                    a |= bit << m
+                rho[a, a] = diag_l[a_l]
+            out[rk] = rho
+        return out, pos
 
     def _ensure_local(self, qubits: Sequence[int], upcoming: List[set]):
         glob = [q for q in qubits if self.slot[q] >= self.nl]
@@ -287,23 +377,37 @@ class DistributedTrajectory:
         ch = 0
         for i, op in enumerate(ops):
             upcoming = uses[i + 1:i + 1 + lookahead]
-            self._ensure_local(op.qubits, upcoming)
-            pos = [self.slot[q] for q in op.qubits]
+            touches_global = any(self.slot[q] >= self.nl for q in op.qubits)
             if not hasattr(op, "kraus"):
-                self.pending.append((pos, np.asarray(op.matrix, np.complex128)))
+                M = np.asarray(op.matrix, np.complex128)
+                if touches_global and _is_diag(M):
+                    self._push_diag_global(op.qubits, M)
+                else:
+                    self._ensure_local(op.qubits, upcoming)
+                    self._push([self.slot[q] for q in op.qubits], M)
                 continue
             u = qtraj.draw(seed, ch, PURPOSE_CHANNEL, traj, 0)
             pick, r, sc = qtraj.channel_first_loop(op.kraus, u, self.mode)
-            if pick >= 0:
-                M = np.asarray(op.kraus[pick], np.complex128) * sc
-                if not _is_identity(M):
-                    self.pending.append((pos, M))
-            else:
+            if pick < 0:
+                # conventional: Alg. 2 lines 13-21 on rho_Q of the unnormalized state
                 self._flush()
-                rho = {rk: self.b.reduce_rho(self.states[rk], pos) for rk in self.f.local_ranks}
+                if touches_global and all(_is_diag(np.conj(np.asarray(K)).T @ np.asarray(K)) for K in op.kraus):
+                    # every K_i^dag K_i diagonal: only the diagonal of rho_Q is needed,
+                    # which each rank holds for its own global-bit values (no swap)
+                    rho, pos = self._rho_diag_global(op.qubits)
+                else:
+                    self._ensure_local(op.qubits, upcoming)
+                    pos = [self.slot[q] for q in op.qubits]
+                    rho = {rk: self.b.reduce_rho(self.states[rk], pos) for rk in self.f.local_ranks}
                 tot = self.f.allreduce(rho)
-                pick, scale = qtraj.channel_choose(op.kraus, pos, tot, r, self.mode)
-                self.pending.append((pos, np.asarray(op.kraus[pick], np.complex128) * scale))
+                pick, sc = qtraj.channel_choose(op.kraus, pos, tot, r, self.mode)
+            M = np.asarray(op.kraus[pick], np.complex128) * sc
+            if not _is_identity(M):
+                if any(self.slot[q] >= self.nl for q in op.qubits) and _is_diag(M):
+                    self._push_diag_global(op.qubits, M)
+                else:
+                    self._ensure_local(op.qubits, upcoming)
+                    self._push([self.slot[q] for q in op.qubits], M)
             kraus_rec.append(pick)
             ch += 1
         self._flush()
