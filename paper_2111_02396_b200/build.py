@@ -6,13 +6,15 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libqtraj.so")
-OBJ = os.path.join(HERE, "build_obj")
+OUT = os.environ.get("QT_LIB_OUT", os.path.join(HERE, "libqtraj.so"))
+OBJ = os.path.join(HERE, "build_obj" + os.environ.get("QT_OBJ_SUFFIX", ""))
 SOURCES = ["tile_pass_r4.cu", "tile_pass_r5.cu", "tile_pass_r6.cu", "tile_pass_tc.cu", "kernels.cu",
            "circuit.cpp", "planner.cpp", "runtime.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"]
+# experiment builds: QT_EXTRA_FLAGS="-DQT_TC_EXP=1" QT_LIB_OUT=... QT_OBJ_SUFFIX=_exp
+FLAGS += os.environ.get("QT_EXTRA_FLAGS", "").split()
 
 
 def _deps():

@@ -528,11 +528,32 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
                 if (std::abs(hop->mats[e] - target) > 1e-15) ident = false;
             }
             v.identity = ident;
+            // qt_add_matrix operations may have any norm: Frobenius bound unless unitary
+            const cd* m = hop->mats.data();
+            if (!(max_dev_from_identity_of_gram(d, &m, 1) < 1e-9)) {
+                double fro = 0;
+                for (int e = 0; e < d * d; ++e) fro += std::norm(hop->mats[e]);
+                v.norm = std::max(1.0, std::sqrt(fro));
+            }
             P.vars.push_back(v);
             P.var_desc.push_back(vd);
         }
         P.ops.push_back(std::move(po));
     }
+    // the f16 tensor-core operands hold matrix entries below 65504: matrices of
+    // huge norm (only possible through qt_add_matrix) use the CUDA-core path
+    if (P.tc)
+        for (const Variant& v : P.vars)
+            if (v.norm > 1e3) {
+                if (o.tensor_cores > 0) {
+                    delete hp;
+                    return fail(QT_EINVAL, "tensor_cores: a matrix of norm > 1e3 does not fit the f16 operands");
+                }
+                P.tc = false;
+                P.R = std::max(f <= 4 ? 4 : f, max_arity);
+                P.f = std::min(f, P.R);
+                break;
+            }
     P.n_channels = chan;
     P.n_recorded = rec;
     P.has_p00 = !C.p00.empty();

@@ -33,19 +33,34 @@ struct PassDesc {
 // (m < k: the gate's qubits ascending, so matrix bit m <-> register bit m;
 // m >= k: filler bits), thread-index bit i <-> tile-local bit tpos[i].
 // 4 bits per entry.
+//
+// Tensor-core gates (kGateTC, 4 qubits) form RUNS inside a pass: the first
+// gate of a run (kGateRunStart) converts the fp32 tile to the f16 hi/lo GEMM
+// operand layout of tc_common.cuh (with a power-of-two tile scale, 2^-shift
+// extra headroom for norm-increasing matrices), and every gate of the run
+// writes its output directly in the operand layout of the next gate: xu[r]
+// is the byte offset, in the next gate's operand layout, of this gate's
+// layout role r (r < 4: matrix bit r, r = 4: group bit, r = 5 + i: thread
+// bit i).  The last gate of a run writes the fp32 tile back.
 struct GateDesc {
     int32_t mat_off;      // complex64 offset into the matrix pool (16-byte aligned)
-    int32_t k;
+    int32_t k;            // arity | kGateTC | kGateRunStart | shift << 16
     uint32_t rpos;
     uint32_t tpos;
+    uint16_t xu[12];      // TC runs: next-gate operand offsets of this gate's roles
+    uint32_t pad[2];
 };
+static_assert(sizeof(GateDesc) == 48, "GateDesc layout");
 
 // Largest number of fused gates in one pass (descriptors staged in smem).
-constexpr int kMaxPassGates = 256;
+constexpr int kMaxPassGates = 64;
 
 // GateDesc::k / FusedDesc::k flag: a (4- or 5-qubit padded) gate applied on
-// tensor cores whose pool entry is the tf32 hi/lo GEMM operand W (tc_common.cuh).
+// tensor cores whose pool entry is the GEMM operand W (tc_common.cuh).
 constexpr int32_t kGateTC = 0x100;
+constexpr int32_t kGateRunStart = 0x200;  // first gate of a tensor-core run
+constexpr int32_t kGateF16 = 0x400;       // 4-qubit gate of a run of >= 2: f16 operands (else 3xTF32)
+constexpr int kGateShiftBit = 16;         // bits 16..23: run scale headroom (log2)
 
 // A conventional channel occurrence (Alg. 2 lines 12-21).
 struct EventDesc {

@@ -55,6 +55,7 @@ struct PlanOp {
 struct Variant {
     int nq = 0;
     bool identity = false;
+    double norm = 1.0;  // upper bound on the spectral norm (1 for unitaries and Kraus operators)
 };
 
 struct Plan {

@@ -20,6 +20,7 @@
 // Reductions never use floating-point atomics: every sum has a fixed order
 // that depends only on n and T, so results are bit-reproducible and
 // independent of batch size and GPU count.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -102,10 +103,31 @@ materialize_kernel(const FusedDesc* __restrict__ fused, const ConsDesc* __restri
         for (int rr = 0; rr < D; ++rr) pool[F.mat_off + rr * D + c] = make_float2((float)v[rr].x, (float)v[rr].y);
         return;
     }
-    // tensor-core operand W (tc_common.cuh): W[2c + a][2j + b] = real 2x2 block of
+    const int k = F.k & 0xff;
+    if (k == 4 && (F.k & kGateF16)) {
+        // kind::f16 operand B (tc_common.cuh): B[2j + b][4c + q] = hi(blk[q & 1][b]),
+        // B[32 + 2j + b][4c + q] = lo(blk[q & 1][b]) for q < 2, 0 for q >= 2, with
+        // blk the real 2x2 block of U[j][c] (input component a, output component b).
+        // Column c of U = v.
+        __half* B = reinterpret_cast<__half*>(pool + F.mat_off);
+        for (int j = 0; j < D; ++j) {
+            const double ur = v[j].x, ui = v[j].y;
+            const double blk[2][2] = {{ur, ui}, {-ui, ur}};
+            for (int b = 0; b < 2; ++b)
+                for (int q = 0; q < 4; ++q) {
+                    const double w = blk[q & 1][b];
+                    const __half h = __double2half(w);
+                    const __half l = __double2half(w - (double)__half2float(h));
+                    const int kk = 4 * c + q;
+                    B[tc::sw128_offset(2 * j + b, 2 * kk) >> 1] = h;
+                    B[tc::sw128_offset(32 + 2 * j + b, 2 * kk) >> 1] = q < 2 ? l : __float2half(0.f);
+                }
+        }
+        return;
+    }
+    // 3xTF32 operand W (tc_common.cuh; 5 qubits, and 4-qubit single-gate runs): W[2c + a][2j + b] = real 2x2 block of
     // U[j][c], stored K-major swizzled as hi then lo tf32 parts.  Column c of U = v.
     uint32_t* W = reinterpret_cast<uint32_t*>(pool + F.mat_off);
-    const int k = F.k & 0xff;
     const uint32_t part = (uint32_t)tc::w_part_bytes(k) >> 2;
     for (int j = 0; j < D; ++j) {
         const double ur = v[j].x, ui = v[j].y;

@@ -16,6 +16,7 @@ struct TileArgs {
     const PassDesc* passes;
     const int32_t* pass_start;  // per slot
     const int32_t* pass_count;  // per slot
+    const int32_t* slots = nullptr;  // grid.y -> slot (the slots active at this step), or nullptr: identity
     const GateDesc* gates;
     float2* pool;               // complex64 matrix pool (read by passes, written by choose)
     const EventDesc* events;

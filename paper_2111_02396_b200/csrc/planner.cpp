@@ -288,6 +288,110 @@ void gate_layout(uint64_t gate_mask, uint64_t S, int T, int R, uint32_t& rpos, u
         if (!((regmask >> p) & 1u)) tpos |= (uint32_t)p << (4 * i++);
 }
 
+// Byte offset of tile bit b in the f16 operand layout of a 4-qubit tensor-core
+// gate (tile_pass_kernel.cuh a_offset): matrix bit m -> 8 << m, group bit
+// (rpos[4]) -> 16 KB, thread bit i -> row bit i of the SWIZZLE_128B layout.
+uint32_t operand_unit(const GateDesc& gd, int b) {
+    for (int m = 0; m < 5; ++m)
+        if ((int)((gd.rpos >> (4 * m)) & 15u) == b) return m < 4 ? 8u << m : 16384u;
+    for (int i = 0; i < 7; ++i)
+        if ((int)((gd.tpos >> (4 * i)) & 15u) == b) return i < 3 ? ((128u << i) ^ (16u << i)) : (128u << i);
+    return 0;
+}
+
+// Bank vector (shared-memory address bits 3..6 of an 8-byte amplitude) of tile
+// bit b in the layout a gate's outputs are written to: the next gate's f16
+// operand layout (matrix bit m -> address bit 3 + m, thread bit i < 3 -> address
+// bit 4 + i, other roles leave the bank unchanged) or, with nx == nullptr, the
+// swizzled fp32 tile (tile bit b -> swizzle bit b mod 4).
+unsigned bank_vec(const GateDesc* nx, int b) {
+    if (!nx) return 1u << (b & 3);
+    for (int m = 0; m < 4; ++m)
+        if ((int)((nx->rpos >> (4 * m)) & 15u) == b) return 1u << m;
+    for (int i = 0; i < 3; ++i)
+        if ((int)((nx->tpos >> (4 * i)) & 15u) == b) return 2u << i;
+    return 0;
+}
+
+// Thread-bit order of a tensor-core gate: the four lowest thread bits (a
+// half-warp's lanes) get tile bits whose bank vectors in the output layout are
+// linearly independent, so the half-warp's 8-byte stores of one configuration
+// hit 16 distinct bank pairs; the group bit is the highest remaining tile bit.
+void tc_relayout(GateDesc& gd, const GateDesc* nx, int T) {
+    uint32_t cfg = 0;
+    for (int m = 0; m < 4; ++m) cfg |= 1u << ((gd.rpos >> (4 * m)) & 15u);
+    int lanes[12], nl = 0;
+    unsigned basis[4] = {0, 0, 0, 0};  // GF(2) basis by leading bit
+    uint32_t used = cfg;
+    for (int b = 0; b < T && nl < 4; ++b) {
+        if ((used >> b) & 1u) continue;
+        unsigned v = bank_vec(nx, b);
+        for (int j = 3; j >= 0 && v; --j)
+            if ((v >> j) & 1u) {
+                if (!basis[j]) {
+                    basis[j] = v;
+                    break;
+                }
+                v ^= basis[j];
+            }
+        if (!v) continue;
+        lanes[nl++] = b;
+        used |= 1u << b;
+    }
+    int grp = -1;
+    for (int b = T - 1; b >= 0; --b)
+        if (!((used >> b) & 1u)) {
+            grp = b;
+            break;
+        }
+    used |= 1u << grp;
+    for (int b = 0; b < T; ++b)
+        if (!((used >> b) & 1u)) lanes[nl++] = b;
+    gd.rpos = (gd.rpos & 0xffffu) | ((uint32_t)grp << 16);
+    gd.tpos = 0;
+    for (int i = 0; i < nl; ++i) gd.tpos |= (uint32_t)lanes[i] << (4 * i);
+}
+
+// Tensor-core runs of one pass (desc.hpp GateDesc): a run starts at the first
+// tensor-core gate, after a CUDA-core gate, or when the product of the runs'
+// norm bounds would exceed 16 (the f16 tile scale has 2^2.5 headroom beyond
+// contractions, widened by 2^shift); layouts are chosen last gate first for
+// conflict-free stores into the next layout; xu = next-gate operand offsets
+// of this gate's roles when the run continues.
+void tc_runs(GateDesc* gd, const double* norms, int count, int T) {
+    int first = -1;
+    double cum = 1.0;
+    for (int g = 0; g < count; ++g) {
+        if (!(gd[g].k & kGateTC)) {
+            first = -1;
+            continue;
+        }
+        if (first < 0 || cum * norms[g] > 16.0) {
+            first = g;
+            cum = 1.0;
+            gd[g].k |= kGateRunStart;
+        }
+        cum *= norms[g];
+        const int shift = cum > 1.0 ? std::min(100, (int)std::ceil(std::log2(cum))) : 0;
+        gd[first].k = (gd[first].k & ~(0xff << kGateShiftBit)) | (shift << kGateShiftBit);
+    }
+    auto chained = [&](int g) {
+        return g + 1 < count && (gd[g].k & kGateTC) && (gd[g + 1].k & (kGateTC | kGateRunStart)) == kGateTC;
+    };
+    // runs of one gate keep the 3xTF32 path (no operand-layout conversion)
+    for (int g = 0; g < count; ++g)
+        if ((gd[g].k & kGateTC) && (chained(g) || (g > 0 && chained(g - 1)))) gd[g].k |= kGateF16;
+    for (int g = count - 1; g >= 0; --g)
+        if (gd[g].k & kGateF16) tc_relayout(gd[g], chained(g) ? &gd[g + 1] : nullptr, T);
+    for (int g = 0; g < count; ++g) {
+        if (!chained(g)) continue;
+        for (int r = 0; r < 12; ++r) {
+            const int b = r < 5 ? (int)((gd[g].rpos >> (4 * r)) & 15u) : (int)((gd[g].tpos >> (4 * (r - 5))) & 15u);
+            gd[g].xu[r] = (uint16_t)operand_unit(gd[g + 1], b);
+        }
+    }
+}
+
 }  // namespace
 
 qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const ObsGroups& og,
@@ -345,6 +449,8 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
     const uint64_t lowT = low_mask(T);
     int32_t pool = 0;
     std::vector<uint64_t> gate_masks;  // parallel to out.gates
+    std::vector<double> gate_norms;    // parallel to out.gates: spectral-norm bound
+    std::vector<int> gate_fused;       // parallel to out.gates: FusedDesc index or -1
     auto alloc = [&](int d2) {
         const int32_t off = pool;
         pool += (d2 + 1) & ~1;  // keep 16-byte alignment
@@ -403,8 +509,12 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
             for (int i : chosen) {
                 FusedGate& g = fg[i];
                 GateDesc gd;
+                std::memset(&gd, 0, sizeof gd);
                 gd.k = popc(g.mask);
                 gd.rpos = gd.tpos = 0;  // after S is final
+                double gnorm = 1.0;
+                for (int it : g.items)
+                    if (items[it].var >= 0) gnorm *= P.vars[items[it].var].norm;
                 if (g.special_event >= 0) {
                     const int d = 1 << gd.k;
                     gd.mat_off = alloc(d * d);
@@ -445,6 +555,8 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
                 if (P.tc && (gd.k & kGateTC)) gd.k = P.tc_k | kGateTC;
                 out.gates.push_back(gd);
                 gate_masks.push_back(g.mask);
+                gate_norms.push_back(gnorm);
+                gate_fused.push_back(g.special_event >= 0 ? -1 : (int)out.fused.size() - 1);
             }
             seg_pass_idx.push_back(out.passes.size());
             out.passes.push_back(pd);
@@ -475,6 +587,11 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
             for (int g = 0; g < pd.gate_count; ++g) {
                 GateDesc& gd = out.gates[pd.gate_begin + g];
                 gate_layout(gate_masks[pd.gate_begin + g], pd.tile_mask, T, P.R, gd.rpos, gd.tpos);
+            }
+            if (P.tc && P.tc_k == 4) {
+                tc_runs(out.gates.data() + pd.gate_begin, gate_norms.data() + pd.gate_begin, pd.gate_count, T);
+                for (int g = 0; g < pd.gate_count; ++g)
+                    if (out.gates[pd.gate_begin + g].k & kGateF16) out.fused[gate_fused[pd.gate_begin + g]].k |= kGateF16;
             }
         }
     }

@@ -11,6 +11,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
+#include <cstdio>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -87,7 +90,7 @@ struct HostBuf {
 // Per-batch device + staging buffers (two of them for pipelining).
 struct BatchBufs {
     DevBuf pass_start, pass_count, passes, gates, fused, cons, events, pool, records, traj_ids,
-        bits, obs_out, status, counters, rho_part, blocksum, obs_part;
+        bits, obs_out, status, counters, rho_part, blocksum, obs_part, slot_list;
     HostBuf h_blob, h_out;
     cudaEvent_t done = nullptr;
     bool inflight = false;
@@ -98,7 +101,7 @@ struct BatchBufs {
     void release() {
         for (DevBuf* b : {&pass_start, &pass_count, &passes, &gates, &fused, &cons, &events, &pool,
                           &records, &traj_ids, &bits, &obs_out, &status, &counters, &rho_part,
-                          &blocksum, &obs_part})
+                          &blocksum, &obs_part, &slot_list})
             b->release();
         h_blob.release();
         h_out.release();
@@ -115,6 +118,7 @@ struct qt_ctx_s {
     BatchBufs bb[2];
     DevBuf vars, var_data, chans, chan_data, obs, p00, p11;
     std::vector<cudaEvent_t> prof_ev;
+    std::vector<std::array<int, 5>> prof_meta;  // per timed launch: step, active slots, gates, TC-f16 gates, rho epilogues
 };
 
 namespace {
@@ -230,7 +234,7 @@ struct CallOut {
 
 // Program concatenation layout (byte offsets into the host blob).
 struct BlobLayout {
-    size_t pass_start, pass_count, passes, gates, fused, cons, events, records, traj_ids, end;
+    size_t pass_start, pass_count, passes, gates, fused, cons, events, records, traj_ids, slot_list, end;
     size_t n_passes, n_gates, n_fused, n_cons, n_events;
     int32_t pool;
     int max_passes;
@@ -272,6 +276,14 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
     L.events = o; o = align16(o + sizeof(EventDesc) * ne);
     L.records = o; o = align16(o + sizeof(int32_t) * (size_t)nslots * std::max(P.n_recorded, 1));
     L.traj_ids = o; o = align16(o + sizeof(uint64_t) * nslots);
+    // per step, the slots whose trajectory still has a pass (launch grid.y)
+    std::vector<int32_t> step_off(maxp + 1, 0);
+    for (int step = 0; step < maxp; ++step) {
+        int act = 0;
+        for (auto& pg : progs) act += step < (int)pg.passes.size();
+        step_off[step + 1] = step_off[step] + act;
+    }
+    L.slot_list = o; o = align16(o + sizeof(int32_t) * std::max(step_off[maxp], 1));
     L.end = o;
     QT_CK(B.h_blob.ensure(L.end));
     char* hb = B.h_blob.as<char>();
@@ -284,6 +296,10 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
     auto* h_ev = reinterpret_cast<EventDesc*>(hb + L.events);
     auto* h_rec = reinterpret_cast<int32_t*>(hb + L.records);
     auto* h_tid = reinterpret_cast<uint64_t*>(hb + L.traj_ids);
+    auto* h_sl = reinterpret_cast<int32_t*>(hb + L.slot_list);
+    for (int step = 0, k = 0; step < maxp; ++step)
+        for (int b = 0; b < nslots; ++b)
+            if (step < (int)progs[b].passes.size()) h_sl[k++] = b;
     size_t bp = 0, bg = 0, bf = 0, bc = 0, be = 0;
     int32_t bpool = 0;
     for (int b = 0; b < nslots; ++b) {
@@ -334,6 +350,7 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
     QT_CK(B.events.ensure(sizeof(EventDesc) * std::max<size_t>(ne, 1)));
     QT_CK(B.records.ensure(sizeof(int32_t) * (size_t)nslots * std::max(P.n_recorded, 1)));
     QT_CK(B.traj_ids.ensure(sizeof(uint64_t) * nslots));
+    QT_CK(B.slot_list.ensure(sizeof(int32_t) * std::max(step_off[maxp], 1)));
     QT_CK(B.pool.ensure(sizeof(float2) * std::max<int32_t>(pool, 2)));
     QT_CK(B.status.ensure(sizeof(int32_t) * nslots));
     QT_CK(B.counters.ensure(sizeof(int32_t) * nslots));
@@ -359,6 +376,7 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
     if ((e = h2d(B.events, L.events, sizeof(EventDesc) * ne)) != QT_OK) return e;
     if ((e = h2d(B.records, L.records, sizeof(int32_t) * (size_t)nslots * P.n_recorded)) != QT_OK) return e;
     if ((e = h2d(B.traj_ids, L.traj_ids, sizeof(uint64_t) * nslots)) != QT_OK) return e;
+    if ((e = h2d(B.slot_list, L.slot_list, sizeof(int32_t) * step_off[maxp])) != QT_OK) return e;
     QT_CK(cudaMemsetAsync(B.status.p, 0, sizeof(int32_t) * nslots, s));
     QT_CK(cudaMemsetAsync(B.counters.p, 0, sizeof(int32_t) * nslots, s));
     // |0...0> in every slot
@@ -389,17 +407,29 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
     A.n_obs = n_obs;
     A.obs = ctx->obs.as<ObsDesc>();
     for (int step = 0; step < maxp; ++step) {
+        const int act = step_off[step + 1] - step_off[step];
+        A.slots = B.slot_list.as<int32_t>() + step_off[step];
         if (profile) {
             cudaEvent_t e0, e1;
             QT_CK(cudaEventCreate(&e0));
             QT_CK(cudaEventCreate(&e1));
             QT_CK(cudaEventRecord(e0, s));
-            QT_CK(launch_tile_pass(A, P.R, P.tc ? P.tc_k : 0, step, ntiles, nslots, s));
+            QT_CK(launch_tile_pass(A, P.R, P.tc ? P.tc_k : 0, step, ntiles, act, s));
             QT_CK(cudaEventRecord(e1, s));
             ctx->prof_ev.push_back(e0);
             ctx->prof_ev.push_back(e1);
+            std::array<int, 5> m{step, 0, 0, 0, 0};
+            for (auto& pg : progs)
+                if (step < (int)pg.passes.size()) {
+                    const PassDesc& pd = pg.passes[step];
+                    ++m[1];
+                    m[2] += pd.gate_count;
+                    m[4] += (pd.flags & kPassRho) != 0;
+                    for (int g = 0; g < pd.gate_count; ++g) m[3] += (pg.gates[pd.gate_begin + g].k & kGateF16) != 0;
+                }
+            ctx->prof_meta.push_back(m);
         } else {
-            QT_CK(launch_tile_pass(A, P.R, P.tc ? P.tc_k : 0, step, ntiles, nslots, s));
+            QT_CK(launch_tile_pass(A, P.R, P.tc ? P.tc_k : 0, step, ntiles, act, s));
         }
         ++launches;
     }
@@ -559,6 +589,7 @@ qt_status qt_run_trajectories(qt_ctx ctx, qt_plan plan, const qt_run_opts* opts,
                     sizeof(ObsDesc) * obs_table.size() + sizeof(double) * (P.p00.size() + P.p11.size());
     for (auto ev : ctx->prof_ev) cudaEventDestroy(ev);
     ctx->prof_ev.clear();
+    ctx->prof_meta.clear();
     const CallOut out{out_bits, out_kraus, out_obs};
     double plan_ms = 0;
     float2* state = reinterpret_cast<float2*>(state_dev);
@@ -609,6 +640,18 @@ qt_status qt_run_trajectories(qt_ctx ctx, qt_plan plan, const qt_run_opts* opts,
         }
         st.pass_kernel_ms = pm;
         st.pass_launches = ctx->prof_ev.size() / 2;
+        // diagnostics: per-launch times and pass composition
+        if (const char* dump = std::getenv("QT_PROFILE_DUMP")) {
+            if (FILE* f = std::fopen(dump, "a")) {
+                for (size_t i = 0; i + 1 < ctx->prof_ev.size() && i / 2 < ctx->prof_meta.size(); i += 2) {
+                    float x = 0;
+                    cudaEventElapsedTime(&x, ctx->prof_ev[i], ctx->prof_ev[i + 1]);
+                    const auto& m = ctx->prof_meta[i / 2];
+                    std::fprintf(f, "%d %d %d %d %d %.4f\n", m[0], m[1], m[2], m[3], m[4], x);
+                }
+                std::fclose(f);
+            }
+        }
     }
     st.trajectories = opts->traj_count;
     st.plan_ms = plan_ms;

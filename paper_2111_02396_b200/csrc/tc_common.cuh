@@ -1,19 +1,48 @@
 // tc_common.cuh -- tcgen05 / TMEM / mbarrier primitives (inline PTX, sm_100a) used by
 // the tensor-core fused-gate path.
 //
-// A fused 4-qubit gate U (16 x 16 complex) applied to 256 subvectors x_s of a
-// 4096-amplitude tile is the real GEMM  Y~ = X~ W  with
-//   X~[s][2c + re/im] = x_s[c]   (M = 256 rows, K = 32),
-//   W[2c + a][2j + b]  = the real 2x2 block of U[j][c] (N = 32),
-// issued as two M = 128 tcgen05.mma.kind::tf32 groups (A = X~ in TMEM,
-// B = W in shared memory, D in TMEM), each K = 32 split into 4 K-steps of 8.
-// Single precision is kept by 3xTF32: X~ = Xh + Xl, W = Wh + Wl (hi/lo tf32),
-// D = Xh Wh + Xl Wh + Xh Wl (the dropped Xl Wl term is ~2^-24 relative).
+// 4-qubit gates (kind::f16, the K1 default): a fused gate U (16 x 16 complex)
+// applied to the 256 subvectors x_s of a tile is the real GEMM D = A B^T with
+//   A[s][4c + q] = {hi(x_c.re), hi(x_c.im), lo(x_c.re), lo(x_c.im)}[q]   (K = 64 f16)
+//   B[n][4c + q]: n = 2j + b   -> hi(W[c][a][b]) for every q   (x_hi + x_lo times W_hi)
+//                 n = 32+2j+b  -> lo(W[c][a][b]) for q < 2, 0 otherwise   (x_hi times W_lo)
+// with a = q & 1 the input component, b the output component and W[c][a][b] the
+// real 2x2 block of U[j][c]; y_j = D[s][2j + b] + D[s][32 + 2j + b].  hi / lo are
+// the f16 rounding of a value and of its remainder (22 significant bits; the
+// dropped x_lo W_lo term is ~2^-22 relative), the amplitudes carrying a
+// power-of-two tile scale that keeps them inside the f16 range.  M = 128 rows
+// per MMA (two groups), N = 64, four K-steps of 16: 8 MMAs per gate.  A and B
+// both live in shared memory in the SWIZZLE_128B K-major layout (one 128-byte
+// row per subvector / output column, 8-row atoms of 1024 B).
+//
+// 5-qubit gates (kind::tf32, f = 5 plans): U (32 x 32 complex) applied to the
+// 128 subvectors x_s of a tile is the real GEMM  Y~ = X~ W  with
+//   X~[s][2c + re/im] = x_s[c]   (M = 128 rows, K = 64),
+//   W[2c + a][2j + b]  = the real 2x2 block of U[j][c] (N = 64),
+// one tcgen05.mma.kind::tf32 chain (A = X~ in TMEM, B = W in shared memory,
+// D in TMEM), K split into 8 K-steps of 8.  Single precision is kept by
+// 3xTF32: X~ = Xh + Xl, W = Wh + Wl (hi/lo tf32), D = Xh Wh + Xl Wh + Xh Wl
+// (the dropped Xl Wl term is ~2^-24 relative).
 #pragma once
 #include <stdint.h>
 
 namespace qt {
 namespace tc {
+
+// Byte offset of byte `kb` of row `row` in a SWIZZLE_128B K-major operand
+// (128-byte rows, 16-byte chunk index ^= row % 8, 8-row atoms of 1024 bytes).
+__host__ __device__ __forceinline__ uint32_t sw128_offset(int row, int kb) {
+    return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((((kb >> 4) ^ row) & 7) << 4) + (kb & 15));
+}
+// f16 operand of a 4-qubit gate: B = [64 rows][64 f16] (8 KB); A = two groups of
+// [128 rows][64 f16] (16 KB each).
+constexpr int kF16GateBytes = 64 * 128;
+constexpr int kF16GroupBytes = 128 * 128;
+
+// Instruction descriptor: kind::f16 (A, B f16, D f32, both K-major), M = 128, N.
+__host__ __device__ constexpr uint32_t idesc_f16_m128(int N) {
+    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
+}
 
 // W in shared memory: [N = 32 rows][K = 32 tf32] K-major, 128-byte rows,
 // SWIZZLE_128B (16-byte chunk index ^= row % 8), 8-row atoms of 1024 bytes.
@@ -73,6 +102,16 @@ __device__ __forceinline__ void mma_tf32_ts_n(uint32_t d_tmem, uint32_t a_tmem, 
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}\n"
         ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate),
           "r"(0u), "r"(0u), "r"(0u), "r"(0u));
+}
+
+// D (TMEM) (+)= A (smem desc) * B (smem desc)^T, kind::f16.
+__device__ __forceinline__ void mma_f16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
+        ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* mbar) {

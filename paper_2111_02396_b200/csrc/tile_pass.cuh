@@ -111,6 +111,64 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
     }
 }
 
+// Block sums of N doubles with one pair of barriers per chunk of 64 / warps
+// values (every thread returns the totals in v).  Fixed summation order.
+template <int NT, int N>
+__device__ __forceinline__ void block_sum_n(double (&v)[N], double* red) {
+    constexpr int W = NT < 32 ? NT : 32;
+    constexpr unsigned mask = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int o = W / 2; o > 0; o >>= 1) v[i] += __shfl_xor_sync(mask, v[i], o);
+    constexpr int NW = (NT + 31) / 32;
+    if constexpr (NW > 1) {
+        constexpr int C = 64 / NW;  // values per chunk (red holds 64 doubles)
+        const int tid = threadIdx.x;
+#pragma unroll
+        for (int c0 = 0; c0 < N; c0 += C) {
+            __syncthreads();
+            if ((tid & 31) == 0)
+#pragma unroll
+                for (int i = c0; i < N && i < c0 + C; ++i) red[(tid >> 5) * C + (i - c0)] = v[i];
+            __syncthreads();
+#pragma unroll
+            for (int i = c0; i < N && i < c0 + C; ++i) {
+                double s = 0.0;
+#pragma unroll
+                for (int w = 0; w < NW; ++w) s += red[w * C + (i - c0)];
+                v[i] = s;
+            }
+        }
+    }
+}
+
+// w[i] for a block-uniform runtime index (jump table, no local memory).
+template <int N>
+__device__ __forceinline__ float pick_uniform(const float (&w)[N], int i) {
+    float r = 0.f;
+#define QT_PICK_CASE(j) \
+    case j:             \
+        if constexpr (j < N) r = w[j]; \
+        break;
+    switch (i) {
+        QT_PICK_CASE(0) QT_PICK_CASE(1) QT_PICK_CASE(2) QT_PICK_CASE(3) QT_PICK_CASE(4) QT_PICK_CASE(5)
+        QT_PICK_CASE(6) QT_PICK_CASE(7) QT_PICK_CASE(8) QT_PICK_CASE(9) QT_PICK_CASE(10) QT_PICK_CASE(11)
+        QT_PICK_CASE(12) QT_PICK_CASE(13) QT_PICK_CASE(14) QT_PICK_CASE(15) QT_PICK_CASE(16) QT_PICK_CASE(17)
+        QT_PICK_CASE(18) QT_PICK_CASE(19) QT_PICK_CASE(20) QT_PICK_CASE(21) QT_PICK_CASE(22) QT_PICK_CASE(23)
+        QT_PICK_CASE(24) QT_PICK_CASE(25) QT_PICK_CASE(26) QT_PICK_CASE(27) QT_PICK_CASE(28) QT_PICK_CASE(29)
+        QT_PICK_CASE(30) QT_PICK_CASE(31) QT_PICK_CASE(32) QT_PICK_CASE(33) QT_PICK_CASE(34) QT_PICK_CASE(35)
+        QT_PICK_CASE(36) QT_PICK_CASE(37) QT_PICK_CASE(38) QT_PICK_CASE(39) QT_PICK_CASE(40) QT_PICK_CASE(41)
+        QT_PICK_CASE(42) QT_PICK_CASE(43) QT_PICK_CASE(44) QT_PICK_CASE(45) QT_PICK_CASE(46) QT_PICK_CASE(47)
+        QT_PICK_CASE(48) QT_PICK_CASE(49) QT_PICK_CASE(50) QT_PICK_CASE(51) QT_PICK_CASE(52) QT_PICK_CASE(53)
+        QT_PICK_CASE(54) QT_PICK_CASE(55) QT_PICK_CASE(56) QT_PICK_CASE(57) QT_PICK_CASE(58) QT_PICK_CASE(59)
+        QT_PICK_CASE(60) QT_PICK_CASE(61) QT_PICK_CASE(62) QT_PICK_CASE(63)
+        default: break;
+    }
+#undef QT_PICK_CASE
+    return r;
+}
+
 // ---------------------------------------------------------------------------
 // Fused-gate application in registers.  The thread holds 2^R amplitudes whose
 // register-index bits 0..K-1 are the gate qubits (matrix bit m <-> register
@@ -228,11 +286,10 @@ __device__ __forceinline__ void rho_partial(const float2* tile, uint32_t qlocal,
                 acc[2 * (a * D + b) + 1] += vi[a] * vr[b] - vr[a] * vi[b];
             }
     }
+    block_sum_n<NT, 2 * D * D>(acc, red);
+    if (tid == 0)
 #pragma unroll
-    for (int e = 0; e < 2 * D * D; ++e) {
-        const double s = block_sum<NT>(acc[e], red);
-        if (tid == 0) out[e] = s;
-    }
+        for (int e = 0; e < 2 * D * D; ++e) out[e] = acc[e];
 }
 
 // Alg. 2 lines 13-21 for one conventional channel, single thread.

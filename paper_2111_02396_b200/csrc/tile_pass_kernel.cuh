@@ -5,23 +5,203 @@
 //               registers, one swizzled shared-memory re-layout per gate.
 //   TC = true : T = 12, 128 threads.  Fused gates are padded to 4 qubits and
 //               applied as the real GEMM of tc_common.cuh on tcgen05 tensor
-//               cores (3xTF32, A = amplitudes in TMEM, B = W in shared memory,
-//               D in TMEM); gates flagged non-TC (the device-chosen operators of
-//               conventional channels, k <= 2) use the CUDA-core path with R = 5.
+//               cores: kind::f16 with hi/lo splits, A and B in shared memory,
+//               D in TMEM.  A run of consecutive tensor-core gates keeps the
+//               tile in the f16 operand layout: each gate's epilogue reads D
+//               from TMEM and writes it straight into the next gate's operand
+//               layout (one barrier and one MMA round trip per gate, no
+//               gather).  Gates flagged non-TC (the device-chosen operators of
+//               conventional channels, k <= 2) use the CUDA-core path with
+//               R = 5 on the fp32 tile.  TCK = 5 (f = 5 plans): 3xTF32 with A
+//               in TMEM, one gate at a time.
 #pragma once
-#include "tile_pass.cuh"
+#include <cuda_fp16.h>
 
-// 1: tensor-core gates issue both M-groups in one MMA batch (256 TMEM columns,
-// 2 CTAs / SM); 0: two batches sharing one A buffer (128 columns, 4 CTAs / SM).
-#ifndef QT_TC_ONE_ROUND
-#define QT_TC_ONE_ROUND 0
-#endif
+#include "tile_pass.cuh"
 
 namespace qt {
 
 namespace detail {
 
-// Apply one padded 4-qubit gate on tensor cores.  Thread t owns subvectors
+// Packed fp32 pair arithmetic (sm_100 FADD2 / FMUL2).
+__device__ __forceinline__ uint64_t pk2(float x, float y) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+    return r;
+}
+__device__ __forceinline__ float2 upk2(uint64_t r) {
+    float2 o;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+    return o;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t sub2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+// f16 hi / lo split of a (scaled) complex amplitude x (packed pair): hi = x with
+// the 13 low mantissa bits cleared (exact in f16 above 2^-14; below, the f16
+// rounding error is < 2^-25 absolute against a tile maximum >= 2^6), lo = the
+// exact fp32 remainder rounded to f16.  Returns {hi pair, lo pair}.
+__device__ __forceinline__ uint2 split_f16(uint64_t x) {
+    const float2 xf = upk2(x);
+    const float hr = __uint_as_float(__float_as_uint(xf.x) & 0xFFFFE000u);
+    const float hi = __uint_as_float(__float_as_uint(xf.y) & 0xFFFFE000u);
+    const float2 l = upk2(sub2(x, pk2(hr, hi)));
+    const __half2 h2 = __floats2half2_rn(hr, hi);
+    const __half2 l2 = __floats2half2_rn(l.x, l.y);
+    return make_uint2(*reinterpret_cast<const uint32_t*>(&h2), *reinterpret_cast<const uint32_t*>(&l2));
+}
+
+// Byte offset, in the f16 operand layout of a gate, of subvector row s (thread
+// bits), group g and configuration c (tc_common.cuh: 8 bytes per amplitude).
+__device__ __forceinline__ uint32_t a_offset(uint32_t s, uint32_t g, uint32_t c) {
+    return g * (uint32_t)tc::kF16GroupBytes + (s >> 3) * 1024u + (s & 7u) * 128u + ((((c >> 1) ^ s) & 7u) << 4) +
+           ((c & 1u) << 3);
+}
+
+// fp32 tile layout of a gate (register bit m <-> tile bit rpos[m], thread bit
+// i <-> tile bit tpos[i]): byte offsets of the 16 configurations, of the
+// group bit, and of this thread's base.
+template <int T>
+__device__ __forceinline__ void fp32_layout(const GateDesc& G, uint32_t (&lo)[16], uint32_t& grp, uint32_t& base) {
+    uint32_t unit[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) unit[m] = swz(1u << ((G.rpos >> (4 * m)) & 15u)) << 3;
+    grp = swz(1u << ((G.rpos >> 16) & 15u)) << 3;
+    lo[0] = 0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int x = 0; x < (1 << m); ++x) lo[x + (1 << m)] = lo[x] ^ unit[m];
+    uint32_t tb = 0;
+#pragma unroll
+    for (int i = 0; i < T - 5; ++i) tb |= ((threadIdx.x >> i) & 1u) << ((G.tpos >> (4 * i)) & 15u);
+    base = swz(tb) << 3;
+}
+
+// One tensor-core gate of a run (4 qubits, kind::f16; tc_common.cuh).  Run start
+// (kGateRunStart): gather the fp32 tile in this gate's register layout, pick the
+// power-of-two tile scale (max |component| -> [2^6, 2^7) / 2^shift, so any
+// contraction of the tile stays below 2^13.5 < f16 max) and write the hi / lo
+// operand rows in place.  Then one elected thread issues the 8 MMAs (2 groups
+// x 4 K-steps, N = 64) and every thread reads its D rows (TMEM lane = thread)
+// and writes the 32 outputs either into the next gate's operand layout (run
+// continues: byte offsets from G.xu) or unscaled into the fp32 tile (run end).
+template <int T>
+__device__ __forceinline__ void tc_gate_f16(float2* tile, uint32_t w_smem, const GateDesc& G, const GateDesc* Gn,
+                                            uint32_t tmem, uint64_t* mbar, uint32_t& phase, float& run_scale,
+                                            float& run_inv, double* red) {
+    using namespace tc;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
+    char* const tb8 = reinterpret_cast<char*>(tile);
+    const uint32_t tile_s = (uint32_t)__cvta_generic_to_shared(tile);
+    const int gk = G.k;
+    if (gk & kGateRunStart) {
+        uint32_t lo[16], grp, base;
+        fp32_layout<T>(G, lo, grp, base);
+        float2 v[32];
+        float amax = 0.f;
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                v[16 * g + c] = *reinterpret_cast<const float2*>(tb8 + (base ^ (g ? grp : 0u) ^ lo[c]));
+                amax = fmaxf(amax, fmaxf(fabsf(v[16 * g + c].x), fabsf(v[16 * g + c].y)));
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        float* redf = reinterpret_cast<float*>(red);
+        if (lane == 0) redf[warp] = amax;
+        __syncthreads();  // every fp32 read done (in-place rewrite below) + maxima visible
+        amax = fmaxf(fmaxf(redf[0], redf[1]), fmaxf(redf[2], redf[3]));
+        const int shift = (gk >> kGateShiftBit) & 0xff;
+        int se = 260 - (int)((__float_as_uint(amax) >> 23) & 0xffu) - shift;  // amax * 2^(se - 127) in [2^6, 2^7)
+        se = min(max(se, 1), 253);
+        run_scale = __uint_as_float((uint32_t)se << 23);
+        run_inv = __uint_as_float((uint32_t)(254 - se) << 23);
+        const uint64_t sc2 = pk2(run_scale, run_scale);
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+                *reinterpret_cast<uint2*>(tb8 + a_offset(tid, (uint32_t)g, (uint32_t)c)) =
+                    split_f16(mul2(pk2(v[16 * g + c].x, v[16 * g + c].y), sc2));
+        fence_proxy_async();
+        __syncthreads();
+    }
+    if (tid == 0) {
+        fence_after();
+        constexpr uint32_t idesc = idesc_f16_m128(64);
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+                mma_f16_ss(tmem + 64 * g, smem_desc_sw128(tile_s + g * kF16GroupBytes + ks * 32),
+                           smem_desc_sw128(w_smem + ks * 32), idesc, ks > 0);
+        mma_commit(mbar);
+    }
+    __syncwarp();
+    // output addressing: next operand layout (run continues) or the fp32 tile
+    const bool chain = Gn != nullptr && (Gn->k & (kGateTC | kGateRunStart)) == kGateTC;
+    uint32_t lo[16], obase, ogrp;
+    if (chain) {
+        const uint4 x0 = *reinterpret_cast<const uint4*>(&G.xu[0]);   // xu[0..7]
+        const uint2 x1 = *reinterpret_cast<const uint2*>(&G.xu[8]);   // xu[8..11]
+        const uint32_t xu[12] = {x0.x & 0xffffu, x0.x >> 16, x0.y & 0xffffu, x0.y >> 16,
+                                 x0.z & 0xffffu, x0.z >> 16, x0.w & 0xffffu, x0.w >> 16,
+                                 x1.x & 0xffffu, x1.x >> 16, x1.y & 0xffffu, x1.y >> 16};
+        obase = 0;
+#pragma unroll
+        for (int i = 0; i < 7; ++i)
+            if ((tid >> i) & 1u) obase ^= xu[5 + i];
+        ogrp = xu[4];
+        lo[0] = 0;
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int x = 0; x < (1 << m); ++x) lo[x + (1 << m)] = lo[x] ^ xu[m];
+    } else {
+        fp32_layout<T>(G, lo, ogrp, obase);
+    }
+    mbar_wait(mbar, phase);  // both groups done: the operand rows may be overwritten
+    phase ^= 1u;
+    fence_after();
+    const uint32_t lane_off = (warp * 32u) << 16;
+    const uint64_t inv2 = pk2(run_inv, run_inv);
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        uint32_t h0[32], h1[32];
+        tmem_ld32(tmem + lane_off + 64 * g, h0);
+        tmem_ld32(tmem + lane_off + 64 * g + 32, h1);
+        tmem_wait_ld();
+        const uint32_t b = obase ^ (g ? ogrp : 0u);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            const uint64_t y = add2(pk2(__uint_as_float(h0[2 * c]), __uint_as_float(h0[2 * c + 1])),
+                                    pk2(__uint_as_float(h1[2 * c]), __uint_as_float(h1[2 * c + 1])));
+            if (chain)
+                *reinterpret_cast<uint2*>(tb8 + (b ^ lo[c])) = split_f16(y);
+            else
+                *reinterpret_cast<float2*>(tb8 + (b ^ lo[c])) = upk2(mul2(y, inv2));
+        }
+    }
+    fence_before();
+}
+
+// Apply one padded 4-qubit gate on tensor cores with 3xTF32 (single-gate runs:
+// no operand-layout conversion).  Thread t owns subvectors
 // s = t and t + 128 (register bit 4 = the group bit); register j = 16 g + c.
 __device__ __forceinline__ void apply_tc_gate(float2* tile, uint32_t w_smem, uint32_t pbase,
                                               const uint32_t (&unit)[5], uint32_t tmem, uint64_t* mbar,
@@ -81,42 +261,6 @@ __device__ __forceinline__ void apply_tc_gate(float2* tile, uint32_t w_smem, uin
             *reinterpret_cast<float2*>(tb8 + (b ^ lo[c])) =
                 make_float2(__uint_as_float(v[2 * c]), __uint_as_float(v[2 * c + 1]));
     };
-#if QT_TC_ONE_ROUND
-    // variant: both groups' A in TMEM (A_g hi/lo at [64 + 64 g, 128 + 64 g)),
-    // one MMA batch and one round trip per gate; needs 256 TMEM columns
-    for (int g = 0; g < 2; ++g) {
-        uint32_t hi[32], lw[32];
-        gather(g, hi, lw);
-        tmem_st32(tmem + lane_off + 64 + 64 * g, hi);
-        tmem_st32(tmem + lane_off + 96 + 64 * g, lw);
-    }
-    tmem_wait_st();
-    fence_before();
-    __syncthreads();
-    if (tid == 0) {
-        fence_after();
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-            const uint64_t bh = smem_desc_sw128(w_smem + ks * 32);
-            const uint64_t bl = smem_desc_sw128(w_smem + kWBytes + ks * 32);
-#pragma unroll
-            for (int g = 0; g < 2; ++g) {
-                mma_tf32_ts(tmem + 32 * g, tmem + 64 + 64 * g + ks * 8, bh, ks > 0);
-                mma_tf32_ts(tmem + 32 * g, tmem + 96 + 64 * g + ks * 8, bh, 1);
-                mma_tf32_ts(tmem + 32 * g, tmem + 64 + 64 * g + ks * 8, bl, 1);
-            }
-        }
-        mma_commit(mbar);
-    }
-    __syncwarp();
-    mbar_wait(mbar, phase);
-    phase ^= 1u;
-    fence_after();
-    scatter(0);
-    scatter(1);
-    fence_before();
-    return;
-#endif
     {
         uint32_t hi[32], lw[32];
         gather(0, hi, lw);
@@ -224,20 +368,23 @@ struct TileCfg {
     static constexpr size_t kRedOff = kHoffOff + sizeof(uint64_t) * ((NH + 1) & ~1);
     static constexpr size_t kGdescOff = kRedOff + 64 * sizeof(double);
     static constexpr size_t kMbarOff = kGdescOff + sizeof(GateDesc) * kMaxPassGates;
+    static_assert(!TC || TCK != 4 || tc::gate_bytes(4) == tc::kF16GateBytes, "f16 operand size");
     static constexpr size_t kBytes = kMbarOff + 16 + 1024;  // + alignment slack
 };
 
 template <int T, int R, bool TC, int TCK = 4>
 __global__ void __launch_bounds__(TileCfg<T, R, TC, TCK>::NT,
-                                  TC ? ((TCK == 5 || QT_TC_ONE_ROUND) ? 2 : 4) : ((R <= 4 && T == 12) ? QT_MINB : 1))
+                                  TC ? (TCK == 5 ? 2 : 4) : ((R <= 4 && T == 12) ? QT_MINB : 1))
 tile_pass_kernel(const TileArgs A, const int step) {
     using Cfg = TileCfg<T, R, TC, TCK>;
-    constexpr uint32_t kTmemCols = (TCK == 5 || QT_TC_ONE_ROUND) ? 256 : 128;  // CTAs per SM share 512 columns
+    // TMEM: TCK = 4: f16 runs use D of both groups (2 x 64 columns), 3xTF32 single
+    // gates D0 / D1 / A hi / A lo (4 x 32); TCK = 5: D 64 + A hi/lo 128
+    constexpr uint32_t kTmemCols = TCK == 5 ? 256 : 128;  // CTAs per SM share 512 columns
     constexpr int NT = Cfg::NT;
     constexpr int NA = Cfg::NA;
     constexpr int CL = Cfg::CL;
     constexpr int NH = Cfg::NH;
-    const int slot = blockIdx.y;
+    const int slot = A.slots ? A.slots[blockIdx.y] : (int)blockIdx.y;
     if (step >= A.pass_count[slot]) return;
     const PassDesc P = A.passes[A.pass_start[slot] + step];
 
@@ -280,7 +427,9 @@ tile_pass_kernel(const TileArgs A, const int step) {
     }
 
     // stage the pass's gate descriptors (async) and the tile-offset table
-    for (int c = tid; c < ng; c += NT) cp_async16(gdesc + c, A.gates + P.gate_begin + c);
+    constexpr int kGdChunks = (int)(sizeof(GateDesc) / 16);
+    for (int c = tid; c < ng * kGdChunks; c += NT)
+        cp_async16(reinterpret_cast<uint4*>(gdesc) + c, reinterpret_cast<const uint4*>(A.gates + P.gate_begin) + c);
     cp_async_commit();
     for (int h = tid; h < NH; h += NT) {
         uint64_t o = 0;
@@ -305,28 +454,14 @@ tile_pass_kernel(const TileArgs A, const int step) {
     // issued before the swizzled 8-byte shared stores.  hoff is linear in its
     // index bits: hoff[(t >> 3) + m NT / 8] = hoff[t >> 3] | hoff[m NT / 8].
     constexpr bool kWide = (CL == 4) && (NT >= 8) && (NA >= 2) && (NA <= 32);
-    // measured (n = 30 single-gate passes): register-staged 16-byte loads 61% of
-    // HBM peak vs 8-byte cp.async 68% -> loads stay asynchronous; stores are wide
-    constexpr bool kWideLoad = false;
-    if constexpr (kWideLoad) {
-        const float4* gsrc = reinterpret_cast<const float4*>(st + base + hoff[tid >> 3] + 2 * (tid & 7));
-        float4 v[NA / 2];
+    // 8-byte asynchronous copies: the swizzle keeps amplitude pairs adjacent but
+    // not 16-byte aligned.  (Measured at n = 30: register-staged 16-byte loads
+    // 61% of HBM peak vs async 8-byte copies 68%.)
 #pragma unroll
-        for (int m = 0; m < NA / 2; ++m) v[m] = __ldcs(gsrc + (hoff[m * (NT / 8)] >> 1));
-#pragma unroll
-        for (int m = 0; m < NA / 2; ++m) {
-            const uint32_t L = 2u * (uint32_t)(tid + m * NT);
-            tile[swz(L)] = make_float2(v[m].x, v[m].y);
-            tile[swz(L + 1)] = make_float2(v[m].z, v[m].w);
-        }
-    } else {
-        // 8-byte asynchronous copies (small tiles)
-#pragma unroll
-        for (int m = 0; m < NA; ++m) {
-            const uint32_t L = (uint32_t)(tid + m * NT);
-            const uint64_t g = base + hoff[L >> CL] + (L & ((1u << CL) - 1u));
-            cp_async8(tile + swz(L), st + g);
-        }
+    for (int m = 0; m < NA; ++m) {
+        const uint32_t L = (uint32_t)(tid + m * NT);
+        const uint64_t g = base + hoff[L >> CL] + (L & ((1u << CL) - 1u));
+        cp_async8(tile + swz(L), st + g);
     }
     cp_async_commit();
     cp_async_wait_all();  // gate descriptors (the tile may still be in flight for other threads)
@@ -340,18 +475,33 @@ tile_pass_kernel(const TileArgs A, const int step) {
             cp_async16(mbuf + 16 * c, reinterpret_cast<const char*>(A.pool + gdesc[0].mat_off) + 16 * c);
         cp_async_commit();
     }
+    float run_scale = 1.f, run_inv = 1.f;  // tensor-core run: tile scale (uniform)
     for (int gi = 0; gi < ng; ++gi) {
-        const GateDesc G = gdesc[gi];
+        const GateDesc& G = gdesc[gi];
         cp_async_wait_all();
-        if constexpr (TC) tc::fence_proxy_async();  // cp.async-written W -> tensor-core reads
+        if constexpr (TC) tc::fence_proxy_async();  // cp.async W / st.shared operand -> tensor-core reads
         __syncthreads();  // tile writes of the previous gate + this gate's matrix visible
         if (gi + 1 < ng) {
-            const GateDesc Gn = gdesc[gi + 1];
+            const GateDesc& Gn = gdesc[gi + 1];
             unsigned char* dst = mbuf + ((gi + 1) & 1) * Cfg::kMbufBytes;
-            const int chunks = mat_bytes(Gn) >> 4;
-            for (int c = tid; c < chunks; c += NT)
-                cp_async16(dst + 16 * c, reinterpret_cast<const char*>(A.pool + Gn.mat_off) + 16 * c);
+            const char* src = reinterpret_cast<const char*>(A.pool + Gn.mat_off);
+            if (TC && TCK == 4 && (Gn.k & kGateTC)) {
+                constexpr int kPer = tc::kF16GateBytes / 16 / NT;
+#pragma unroll
+                for (int c = 0; c < kPer; ++c) cp_async16(dst + 16 * (tid + c * NT), src + 16 * (tid + c * NT));
+            } else {
+                const int chunks = mat_bytes(Gn) >> 4;
+                for (int c = tid; c < chunks; c += NT) cp_async16(dst + 16 * c, src + 16 * c);
+            }
             cp_async_commit();
+        }
+        unsigned char* mcur = mbuf + (gi & 1) * Cfg::kMbufBytes;
+        if constexpr (TC && TCK == 4) {
+            if (G.k & kGateF16) {
+                tc_gate_f16<T>(tile, (uint32_t)__cvta_generic_to_shared(mcur), G, gi + 1 < ng ? &gdesc[gi + 1] : nullptr,
+                               tmem, mbar, phase, run_scale, run_inv, red);
+                continue;
+            }
         }
         // register layout (host-computed): register bit m <-> tile bit rpos[m]
         // (bits 0..k-1 = the gate qubits), thread bit i <-> tile bit tpos[i]
@@ -361,7 +511,6 @@ tile_pass_kernel(const TileArgs A, const int step) {
         uint32_t tb = 0;
 #pragma unroll
         for (int i = 0; i < T - R; ++i) tb |= (((uint32_t)tid >> i) & 1u) << ((G.tpos >> (4 * i)) & 15u);
-        unsigned char* mcur = mbuf + (gi & 1) * Cfg::kMbufBytes;
         if constexpr (TC) {
             if (G.k & kGateTC) {
                 if constexpr (R == 5 && TCK == 4)
@@ -428,36 +577,57 @@ tile_pass_kernel(const TileArgs A, const int step) {
         if (tid == 0) A.blocksum[tile_row] = s;
     }
     if (P.flags & kPassObs) {
-        for (int o = 0; o < P.obs_count; ++o) {
-            const ObsDesc O = A.obs[P.obs_begin + o];
-            const uint64_t xo = O.xmask & ~P.tile_mask;
-            const uint32_t xl = to_local<T>(O.xmask, P), zl = to_local<T>(O.zmask, P);
-            const int zs = __popcll(base & O.zmask) & 1;
-            double s = 0.0;
-            if (O.xmask == 0) {  // Z-type string: sum of +-|psi_L|^2 (fp32 per thread, fp64 across)
-                float sf = 0.f;
+        // Z-type strings: p[m] = |psi(tid + m NT)|^2 and its Walsh-Hadamard
+        // transform over the register index m, so a string whose tile-local Z
+        // bits are zt (thread bits) + zm (register bits) contributes
+        // (-1)^{|tid & zt| + |base & z|} w[zm].  fp32 per thread, fp64 across.
+        float w[NA];
 #pragma unroll
-                for (int m = 0; m < NA; ++m) {
-                    const uint32_t L = (uint32_t)(tid + m * NT);
-                    const float2 v = tile[swz(L)];
-                    const float p = fmaf(v.x, v.x, v.y * v.y);
-                    sf += (__popc(L & zl) & 1) ? -p : p;
+        for (int m = 0; m < NA; ++m) {
+            const float2 v = tile[swz((uint32_t)(tid + m * NT))];
+            w[m] = fmaf(v.x, v.x, v.y * v.y);
+        }
+#pragma unroll
+        for (int h = 1; h < NA; h <<= 1)
+#pragma unroll
+            for (int m = 0; m < NA; ++m)
+                if (!(m & h)) {
+                    const float a = w[m], b = w[m | h];
+                    w[m] = a + b;
+                    w[m | h] = a - b;
                 }
-                s = zs ? -(double)sf : (double)sf;
-            } else {
+        constexpr int kChunk = 8;
+        for (int o0 = 0; o0 < P.obs_count; o0 += kChunk) {
+            double part[kChunk];
+#pragma unroll
+            for (int j = 0; j < kChunk; ++j) {
+                part[j] = 0.0;
+                if (o0 + j >= P.obs_count) continue;
+                const ObsDesc O = A.obs[P.obs_begin + o0 + j];
+                const uint32_t zl = to_local<T>(O.zmask, P);
+                const int zs = __popcll(base & O.zmask) & 1;
+                if (O.xmask == 0) {
+                    const float v = pick_uniform<NA>(w, (int)(zl >> (T - R)));
+                    const int par = (__popc((uint32_t)tid & zl & (uint32_t)(NT - 1)) + zs) & 1;
+                    part[j] = par ? -(double)v : (double)v;
+                    continue;
+                }
+                const uint64_t xo = O.xmask & ~P.tile_mask;
+                const uint32_t xl = to_local<T>(O.xmask, P);
+                double s = 0.0;
                 for (int m = 0; m < NA; ++m) {
                     const uint32_t L = (uint32_t)(tid + m * NT);
                     const float2 v = tile[swz(L)];
-                    float2 w;
+                    float2 wv;
                     if (xo == 0) {
-                        w = tile[swz(L ^ xl)];
+                        wv = tile[swz(L ^ xl)];
                     } else {  // partner amplitude in another tile (read-only pass only)
                         const uint64_t g = base + hoff[L >> CL] + (L & ((1u << CL) - 1u));
-                        w = st[g ^ O.xmask];
+                        wv = st[g ^ O.xmask];
                     }
                     // c = conj(w) * v, times i^ny, times (-1)^parity
-                    const double cr = (double)w.x * v.x + (double)w.y * v.y;
-                    const double ci = (double)w.x * v.y - (double)w.y * v.x;
+                    const double cr = (double)wv.x * v.x + (double)wv.y * v.y;
+                    const double ci = (double)wv.x * v.y - (double)wv.y * v.x;
                     double t;
                     switch (O.ny & 3) {
                         case 0: t = cr; break;
@@ -468,9 +638,12 @@ tile_pass_kernel(const TileArgs A, const int step) {
                     const int par = (__popc(L & zl) + zs) & 1;
                     s += par ? -t : t;
                 }
+                part[j] = s;
             }
-            s = block_sum<NT>(s, red);
-            if (tid == 0) A.obs_part[tile_row * A.n_obs + O.slot] = s;
+            block_sum_n<NT, kChunk>(part, red);
+            if (tid == 0)
+                for (int j = 0; j < kChunk && o0 + j < P.obs_count; ++j)
+                    A.obs_part[tile_row * A.n_obs + A.obs[P.obs_begin + o0 + j].slot] = part[j];
         }
     }
 
