@@ -180,7 +180,7 @@ __device__ __forceinline__ void tc_gate_f16(float2* tile, uint32_t w_smem, const
     fence_after();
     const uint32_t lane_off = (warp * 32u) << 16;
     const uint64_t inv2 = pk2(run_inv, run_inv);
-#pragma unroll
+#pragma unroll 1
     for (int g = 0; g < 2; ++g) {
         uint32_t h0[32], h1[32];
         tmem_ld32(tmem + lane_off + 64 * g, h0);
@@ -457,11 +457,21 @@ tile_pass_kernel(const TileArgs A, const int step) {
     // 8-byte asynchronous copies: the swizzle keeps amplitude pairs adjacent but
     // not 16-byte aligned.  (Measured at n = 30: register-staged 16-byte loads
     // 61% of HBM peak vs async 8-byte copies 68%.)
+    // hoff and swz are linear in the index bits: slot L = tid + m NT has global
+    // offset hoff[tid >> CL] + hoff[m NT >> CL] + (tid & (2^CL - 1)) (NT >= 2^CL)
+    if constexpr (NT >= (1 << CL)) {
+        const float2* gsrc = st + base + hoff[tid >> CL] + ((uint32_t)tid & ((1u << CL) - 1u));
+        const uint32_t sb = swz((uint32_t)tid);
+#pragma unroll 8
+        for (int m = 0; m < NA; ++m)
+            cp_async8(tile + (sb ^ swz((uint32_t)(m * NT))), gsrc + hoff[(m * NT) >> CL]);
+    } else {
 #pragma unroll
-    for (int m = 0; m < NA; ++m) {
-        const uint32_t L = (uint32_t)(tid + m * NT);
-        const uint64_t g = base + hoff[L >> CL] + (L & ((1u << CL) - 1u));
-        cp_async8(tile + swz(L), st + g);
+        for (int m = 0; m < NA; ++m) {
+            const uint32_t L = (uint32_t)(tid + m * NT);
+            const uint64_t g = base + hoff[L >> CL] + (L & ((1u << CL) - 1u));
+            cp_async8(tile + swz(L), st + g);
+        }
     }
     cp_async_commit();
     cp_async_wait_all();  // gate descriptors (the tile may still be in flight for other threads)
@@ -596,25 +606,24 @@ tile_pass_kernel(const TileArgs A, const int step) {
                     w[m] = a + b;
                     w[m | h] = a - b;
                 }
-        constexpr int kChunk = 8;
-        for (int o0 = 0; o0 < P.obs_count; o0 += kChunk) {
-            double part[kChunk];
-#pragma unroll
-            for (int j = 0; j < kChunk; ++j) {
-                part[j] = 0.0;
-                if (o0 + j >= P.obs_count) continue;
-                const ObsDesc O = A.obs[P.obs_begin + o0 + j];
-                const uint32_t zl = to_local<T>(O.zmask, P);
-                const int zs = __popcll(base & O.zmask) & 1;
-                if (O.xmask == 0) {
-                    const float v = pick_uniform<NA>(w, (int)(zl >> (T - R)));
-                    const int par = (__popc((uint32_t)tid & zl & (uint32_t)(NT - 1)) + zs) & 1;
-                    part[j] = par ? -(double)v : (double)v;
-                    continue;
-                }
+        // one observable at a time (compact code): warp sums parked in red[],
+        // flushed with one barrier pair per 64 / warps observables
+        constexpr int NW = (NT + 31) / 32;
+        constexpr int kFlush = 64 / NW;
+        for (int o = 0; o < P.obs_count; ++o) {
+            const ObsDesc O = A.obs[P.obs_begin + o];
+            const uint32_t zl = to_local<T>(O.zmask, P);
+            const int zs = __popcll(base & O.zmask) & 1;
+            double part;
+            if (O.xmask == 0) {
+                const float v = pick_uniform<NA>(w, (int)(zl >> (T - R)));
+                const int par = (__popc((uint32_t)tid & zl & (uint32_t)(NT - 1)) + zs) & 1;
+                part = par ? -(double)v : (double)v;
+            } else {
                 const uint64_t xo = O.xmask & ~P.tile_mask;
                 const uint32_t xl = to_local<T>(O.xmask, P);
-                double s = 0.0;
+                part = 0.0;
+#pragma unroll 1
                 for (int m = 0; m < NA; ++m) {
                     const uint32_t L = (uint32_t)(tid + m * NT);
                     const float2 v = tile[swz(L)];
@@ -636,14 +645,25 @@ tile_pass_kernel(const TileArgs A, const int step) {
                         default: t = ci; break;
                     }
                     const int par = (__popc(L & zl) + zs) & 1;
-                    s += par ? -t : t;
+                    part += par ? -t : t;
                 }
-                part[j] = s;
             }
-            block_sum_n<NT, kChunk>(part, red);
-            if (tid == 0)
-                for (int j = 0; j < kChunk && o0 + j < P.obs_count; ++j)
-                    A.obs_part[tile_row * A.n_obs + A.obs[P.obs_begin + o0 + j].slot] = part[j];
+            constexpr int W = NT < 32 ? NT : 32;
+            constexpr unsigned mask = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
+#pragma unroll
+            for (int sh = W / 2; sh > 0; sh >>= 1) part += __shfl_xor_sync(mask, part, sh);
+            const int j = o % kFlush;
+            if ((tid & 31) == 0) red[j * NW + (tid >> 5)] = part;
+            if (j == kFlush - 1 || o + 1 == P.obs_count) {
+                __syncthreads();
+                for (int jj = tid; jj <= j; jj += NT) {
+                    double v = 0.0;
+#pragma unroll
+                    for (int ww = 0; ww < NW; ++ww) v += red[jj * NW + ww];
+                    A.obs_part[tile_row * A.n_obs + A.obs[P.obs_begin + o - j + jj].slot] = v;
+                }
+                __syncthreads();
+            }
         }
     }
 
@@ -651,10 +671,11 @@ tile_pass_kernel(const TileArgs A, const int step) {
     if (P.flags & kPassStore) {
         if constexpr (kWide) {
             float4* gdst = reinterpret_cast<float4*>(st + base + hoff[tid >> 3] + 2 * (tid & 7));
-#pragma unroll
+            const uint32_t sb = swz(2u * (uint32_t)tid);
+#pragma unroll 4
             for (int m = 0; m < NA / 2; ++m) {
-                const uint32_t L = 2u * (uint32_t)(tid + m * NT);
-                const float2 a0 = tile[swz(L)], a1 = tile[swz(L + 1)];
+                const uint32_t a = sb ^ swz(2u * (uint32_t)(m * NT));  // swz(L + 1) = swz(L) ^ 1
+                const float2 a0 = tile[a], a1 = tile[a ^ 1u];
                 gdst[hoff[m * (NT / 8)] >> 1] = make_float4(a0.x, a0.y, a1.x, a1.y);
             }
         } else {
