@@ -25,7 +25,7 @@ struct PassDesc {
     int32_t obs_begin;    // into ObsDesc[] (kPassObs)
     int32_t obs_count;
     uint8_t tq[12];       // global qubit of tile bit i (ascending), i < T
-    int32_t pad;
+    int32_t slot;         // batch slot (set by the executor in the per-step launch arrays)
 };
 
 // A fused gate inside a pass and the register layout used to apply it:

@@ -16,7 +16,8 @@ struct TileArgs {
     const PassDesc* passes;
     const int32_t* pass_start;  // per slot
     const int32_t* pass_count;  // per slot
-    const int32_t* slots = nullptr;  // grid.y -> slot (the slots active at this step), or nullptr: identity
+    const PassDesc* step_passes = nullptr;  // grid.y -> this step's pass of an active slot (.slot), or
+                                            // nullptr: slot = grid.y, pass via pass_start / pass_count
     const GateDesc* gates;
     float2* pool;               // complex64 matrix pool (read by passes, written by choose)
     const EventDesc* events;
@@ -32,6 +33,7 @@ struct TileArgs {
     int n_obs;
     const ObsDesc* obs;
     uint32_t prefetch;          // L2-prefetch the tile this many CTAs ahead (0 = off; set by the launcher)
+    unsigned long long* timing = nullptr;  // -DQT_TIMING builds: clock64 phase sums (diagnostics)
 };
 
 // Largest register width R (amplitudes per thread = 2^R) compiled.

@@ -317,12 +317,12 @@ unsigned bank_vec(const GateDesc* nx, int b) {
 // half-warp's lanes) get tile bits whose bank vectors in the output layout are
 // linearly independent, so the half-warp's 8-byte stores of one configuration
 // hit 16 distinct bank pairs; the group bit is the highest remaining tile bit.
-void tc_relayout(GateDesc& gd, const GateDesc* nx, int T) {
+void tc_relayout(GateDesc& gd, const GateDesc* nx, int T, int grp) {
     uint32_t cfg = 0;
     for (int m = 0; m < 4; ++m) cfg |= 1u << ((gd.rpos >> (4 * m)) & 15u);
     int lanes[12], nl = 0;
     unsigned basis[4] = {0, 0, 0, 0};  // GF(2) basis by leading bit
-    uint32_t used = cfg;
+    uint32_t used = cfg | (1u << grp);
     for (int b = 0; b < T && nl < 4; ++b) {
         if ((used >> b) & 1u) continue;
         unsigned v = bank_vec(nx, b);
@@ -338,13 +338,6 @@ void tc_relayout(GateDesc& gd, const GateDesc* nx, int T) {
         lanes[nl++] = b;
         used |= 1u << b;
     }
-    int grp = -1;
-    for (int b = T - 1; b >= 0; --b)
-        if (!((used >> b) & 1u)) {
-            grp = b;
-            break;
-        }
-    used |= 1u << grp;
     for (int b = 0; b < T; ++b)
         if (!((used >> b) & 1u)) lanes[nl++] = b;
     gd.rpos = (gd.rpos & 0xffffu) | ((uint32_t)grp << 16);
@@ -359,8 +352,14 @@ void tc_relayout(GateDesc& gd, const GateDesc* nx, int T) {
 // conflict-free stores into the next layout; xu = next-gate operand offsets
 // of this gate's roles when the run continues.
 void tc_runs(GateDesc* gd, const double* norms, int count, int T) {
+    auto cfg_of = [&](int g) {
+        uint32_t c = 0;
+        for (int m = 0; m < 4; ++m) c |= 1u << ((gd[g].rpos >> (4 * m)) & 15u);
+        return c;
+    };
     int first = -1;
     double cum = 1.0;
+    const uint32_t all = (1u << T) - 1u;
     for (int g = 0; g < count; ++g) {
         if (!(gd[g].k & kGateTC)) {
             first = -1;
@@ -381,8 +380,25 @@ void tc_runs(GateDesc* gd, const double* norms, int count, int T) {
     // runs of one gate keep the 3xTF32 path (no operand-layout conversion)
     for (int g = 0; g < count; ++g)
         if ((gd[g].k & kGateTC) && (chained(g) || (g > 0 && chained(g - 1)))) gd[g].k |= kGateF16;
+    // group bit: runs are cut into maximal segments whose gates leave a common
+    // tile bit untouched; that bit is the segment's group bit, so inside a
+    // segment the two 128-row groups pipeline independently (K1 tc_run_f16)
+    std::vector<int> grp(count, -1);
+    for (int g = 0; g < count;) {
+        if (!(gd[g].k & kGateF16)) {
+            ++g;
+            continue;
+        }
+        int e = g;
+        uint32_t u = cfg_of(g);
+        while (chained(e) && (u | cfg_of(e + 1)) != all) u |= cfg_of(++e);
+        int b = T - 1;
+        while (b >= 0 && ((u >> b) & 1u)) --b;
+        for (int x = g; x <= e; ++x) grp[x] = b;
+        g = e + 1;
+    }
     for (int g = count - 1; g >= 0; --g)
-        if (gd[g].k & kGateF16) tc_relayout(gd[g], chained(g) ? &gd[g + 1] : nullptr, T);
+        if (gd[g].k & kGateF16) tc_relayout(gd[g], chained(g) ? &gd[g + 1] : nullptr, T, grp[g]);
     for (int g = 0; g < count; ++g) {
         if (!chained(g)) continue;
         for (int r = 0; r < 12; ++r) {
@@ -633,7 +649,7 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
         std::memset(pd.tq, 0, sizeof pd.tq);
         int i = 0;
         for (uint64_t mk = pd.tile_mask; mk; mk &= mk - 1) pd.tq[i++] = (uint8_t)__builtin_ctzll(mk);
-        pd.pad = 0;
+        pd.slot = 0;
     }
     out.pool_size = pool;
     // algorithmic bytes: 2^(n+4) per storing pass, 2^(n+3) per read-only pass

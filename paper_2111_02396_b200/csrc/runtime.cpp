@@ -283,7 +283,7 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
         for (auto& pg : progs) act += step < (int)pg.passes.size();
         step_off[step + 1] = step_off[step] + act;
     }
-    L.slot_list = o; o = align16(o + sizeof(int32_t) * std::max(step_off[maxp], 1));
+    L.slot_list = o; o = align16(o + sizeof(PassDesc) * std::max(step_off[maxp], 1));
     L.end = o;
     QT_CK(B.h_blob.ensure(L.end));
     char* hb = B.h_blob.as<char>();
@@ -296,10 +296,7 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
     auto* h_ev = reinterpret_cast<EventDesc*>(hb + L.events);
     auto* h_rec = reinterpret_cast<int32_t*>(hb + L.records);
     auto* h_tid = reinterpret_cast<uint64_t*>(hb + L.traj_ids);
-    auto* h_sl = reinterpret_cast<int32_t*>(hb + L.slot_list);
-    for (int step = 0, k = 0; step < maxp; ++step)
-        for (int b = 0; b < nslots; ++b)
-            if (step < (int)progs[b].passes.size()) h_sl[k++] = b;
+    auto* h_sl = reinterpret_cast<PassDesc*>(hb + L.slot_list);
     size_t bp = 0, bg = 0, bf = 0, bc = 0, be = 0;
     int32_t bpool = 0;
     for (int b = 0; b < nslots; ++b) {
@@ -340,6 +337,13 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
             st->alg_flops += pg.alg_flops;
         }
     }
+    // per-step launch arrays: this step's (rebased) pass of every active slot
+    for (int step = 0, k = 0; step < maxp; ++step)
+        for (int b = 0; b < nslots; ++b)
+            if (step < (int)progs[b].passes.size()) {
+                h_sl[k] = h_pass[h_ps[b] + step];
+                h_sl[k++].slot = b;
+            }
     // device buffers
     QT_CK(B.pass_start.ensure(sizeof(int32_t) * nslots));
     QT_CK(B.pass_count.ensure(sizeof(int32_t) * nslots));
@@ -350,7 +354,7 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
     QT_CK(B.events.ensure(sizeof(EventDesc) * std::max<size_t>(ne, 1)));
     QT_CK(B.records.ensure(sizeof(int32_t) * (size_t)nslots * std::max(P.n_recorded, 1)));
     QT_CK(B.traj_ids.ensure(sizeof(uint64_t) * nslots));
-    QT_CK(B.slot_list.ensure(sizeof(int32_t) * std::max(step_off[maxp], 1)));
+    QT_CK(B.slot_list.ensure(sizeof(PassDesc) * std::max(step_off[maxp], 1)));
     QT_CK(B.pool.ensure(sizeof(float2) * std::max<int32_t>(pool, 2)));
     QT_CK(B.status.ensure(sizeof(int32_t) * nslots));
     QT_CK(B.counters.ensure(sizeof(int32_t) * nslots));
@@ -376,7 +380,7 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
     if ((e = h2d(B.events, L.events, sizeof(EventDesc) * ne)) != QT_OK) return e;
     if ((e = h2d(B.records, L.records, sizeof(int32_t) * (size_t)nslots * P.n_recorded)) != QT_OK) return e;
     if ((e = h2d(B.traj_ids, L.traj_ids, sizeof(uint64_t) * nslots)) != QT_OK) return e;
-    if ((e = h2d(B.slot_list, L.slot_list, sizeof(int32_t) * step_off[maxp])) != QT_OK) return e;
+    if ((e = h2d(B.slot_list, L.slot_list, sizeof(PassDesc) * step_off[maxp])) != QT_OK) return e;
     QT_CK(cudaMemsetAsync(B.status.p, 0, sizeof(int32_t) * nslots, s));
     QT_CK(cudaMemsetAsync(B.counters.p, 0, sizeof(int32_t) * nslots, s));
     // |0...0> in every slot
@@ -408,7 +412,7 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
     A.obs = ctx->obs.as<ObsDesc>();
     for (int step = 0; step < maxp; ++step) {
         const int act = step_off[step + 1] - step_off[step];
-        A.slots = B.slot_list.as<int32_t>() + step_off[step];
+        A.step_passes = B.slot_list.as<PassDesc>() + step_off[step];
         if (profile) {
             cudaEvent_t e0, e1;
             QT_CK(cudaEventCreate(&e0));

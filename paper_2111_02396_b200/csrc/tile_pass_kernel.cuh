@@ -91,24 +91,39 @@ __device__ __forceinline__ void fp32_layout(const GateDesc& G, uint32_t (&lo)[16
     base = swz(tb) << 3;
 }
 
-// One tensor-core gate of a run (4 qubits, kind::f16; tc_common.cuh).  Run start
-// (kGateRunStart): gather the fp32 tile in this gate's register layout, pick the
-// power-of-two tile scale (max |component| -> [2^6, 2^7) / 2^shift, so any
-// contraction of the tile stays below 2^13.5 < f16 max) and write the hi / lo
-// operand rows in place.  Then one elected thread issues the 8 MMAs (2 groups
-// x 4 K-steps, N = 64) and every thread reads its D rows (TMEM lane = thread)
-// and writes the 32 outputs either into the next gate's operand layout (run
-// continues: byte offsets from G.xu) or unscaled into the fp32 tile (run end).
+// A run of tensor-core gates (4 qubits, kind::f16; tc_common.cuh), gates g0..g1
+// of the pass (returns g1).  Run start: gather the fp32 tile in the first
+// gate's layout, pick the power-of-two tile scale (max |component| -> [2^6,
+// 2^7) / 2^shift, so any contraction of the tile stays below 2^13.5 < f16 max)
+// and write the hi / lo operand rows in place.  The run's group bit is a tile
+// bit no gate touches, so the two 128-row groups are independent pipelines:
+// while the MMAs of one group run, the threads read the other group's D rows
+// (TMEM lane = thread) and write them straight into the next gate's operand
+// layout (byte offsets from G.xu); the last gate writes the fp32 tile back.
 template <int T>
-__device__ __forceinline__ void tc_gate_f16(float2* tile, uint32_t w_smem, const GateDesc& G, const GateDesc* Gn,
-                                            uint32_t tmem, uint64_t* mbar, uint32_t& phase, float& run_scale,
-                                            float& run_inv, double* red) {
+__device__ __forceinline__ int tc_run_f16(float2* tile, unsigned char* mbuf, uint32_t mbuf_bytes,
+                                          const GateDesc* gdesc, int g0, int ng, const float2* pool, uint32_t tmem,
+                                          uint64_t* mbar, uint32_t (&ph)[2], double* red,
+                                          unsigned long long* timing = nullptr) {
     using namespace tc;
+    constexpr int NT = 128;
+#ifdef QT_TIMING
+    const bool ts = timing && (blockIdx.x % 32u) == 7u && threadIdx.x == 0;
+    const int tw = 0;
+    long long tm[7];
+#define QT_MARK(i) tm[i] = clock64()
+#else
+#define QT_MARK(i)
+#endif
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
     char* const tb8 = reinterpret_cast<char*>(tile);
     const uint32_t tile_s = (uint32_t)__cvta_generic_to_shared(tile);
-    const int gk = G.k;
-    if (gk & kGateRunStart) {
+    const uint32_t mbuf_s = (uint32_t)__cvta_generic_to_shared(mbuf);
+    int g1 = g0;
+    while (g1 + 1 < ng && (gdesc[g1 + 1].k & (kGateF16 | kGateRunStart)) == kGateF16) ++g1;
+    float run_inv;
+    {
+        const GateDesc& G = gdesc[g0];
         uint32_t lo[16], grp, base;
         fp32_layout<T>(G, lo, grp, base);
         float2 v[32];
@@ -126,10 +141,10 @@ __device__ __forceinline__ void tc_gate_f16(float2* tile, uint32_t w_smem, const
         if (lane == 0) redf[warp] = amax;
         __syncthreads();  // every fp32 read done (in-place rewrite below) + maxima visible
         amax = fmaxf(fmaxf(redf[0], redf[1]), fmaxf(redf[2], redf[3]));
-        const int shift = (gk >> kGateShiftBit) & 0xff;
+        const int shift = (G.k >> kGateShiftBit) & 0xff;
         int se = 260 - (int)((__float_as_uint(amax) >> 23) & 0xffu) - shift;  // amax * 2^(se - 127) in [2^6, 2^7)
         se = min(max(se, 1), 253);
-        run_scale = __uint_as_float((uint32_t)se << 23);
+        const float run_scale = __uint_as_float((uint32_t)se << 23);
         run_inv = __uint_as_float((uint32_t)(254 - se) << 23);
         const uint64_t sc2 = pk2(run_scale, run_scale);
 #pragma unroll
@@ -141,52 +156,29 @@ __device__ __forceinline__ void tc_gate_f16(float2* tile, uint32_t w_smem, const
         fence_proxy_async();
         __syncthreads();
     }
-    if (tid == 0) {
+    // MMAs of gate g, group grp: D[grp] (TMEM columns 64 grp..) = A[grp] W(g)^T
+    auto issue = [&](int g, int grp) {
         fence_after();
         constexpr uint32_t idesc = idesc_f16_m128(64);
+        const uint32_t w = mbuf_s + (uint32_t)(g & 1) * mbuf_bytes;
 #pragma unroll
-        for (int g = 0; g < 2; ++g)
-#pragma unroll
-            for (int ks = 0; ks < 4; ++ks)
-                mma_f16_ss(tmem + 64 * g, smem_desc_sw128(tile_s + g * kF16GroupBytes + ks * 32),
-                           smem_desc_sw128(w_smem + ks * 32), idesc, ks > 0);
-        mma_commit(mbar);
+        for (int ks = 0; ks < 4; ++ks)
+            mma_f16_ss(tmem + 64 * grp, smem_desc_sw128(tile_s + grp * kF16GroupBytes + ks * 32),
+                       smem_desc_sw128(w + ks * 32), idesc, ks > 0);
+        mma_commit(mbar + grp);
+    };
+    if (tid == 0) {
+        issue(g0, 0);
+        issue(g0, 1);
     }
     __syncwarp();
-    // output addressing: next operand layout (run continues) or the fp32 tile
-    const bool chain = Gn != nullptr && (Gn->k & (kGateTC | kGateRunStart)) == kGateTC;
-    uint32_t lo[16], obase, ogrp;
-    if (chain) {
-        const uint4 x0 = *reinterpret_cast<const uint4*>(&G.xu[0]);   // xu[0..7]
-        const uint2 x1 = *reinterpret_cast<const uint2*>(&G.xu[8]);   // xu[8..11]
-        const uint32_t xu[12] = {x0.x & 0xffffu, x0.x >> 16, x0.y & 0xffffu, x0.y >> 16,
-                                 x0.z & 0xffffu, x0.z >> 16, x0.w & 0xffffu, x0.w >> 16,
-                                 x1.x & 0xffffu, x1.x >> 16, x1.y & 0xffffu, x1.y >> 16};
-        obase = 0;
-#pragma unroll
-        for (int i = 0; i < 7; ++i)
-            if ((tid >> i) & 1u) obase ^= xu[5 + i];
-        ogrp = xu[4];
-        lo[0] = 0;
-#pragma unroll
-        for (int m = 0; m < 4; ++m)
-#pragma unroll
-            for (int x = 0; x < (1 << m); ++x) lo[x + (1 << m)] = lo[x] ^ xu[m];
-    } else {
-        fp32_layout<T>(G, lo, ogrp, obase);
-    }
-    mbar_wait(mbar, phase);  // both groups done: the operand rows may be overwritten
-    phase ^= 1u;
-    fence_after();
     const uint32_t lane_off = (warp * 32u) << 16;
-    const uint64_t inv2 = pk2(run_inv, run_inv);
-#pragma unroll 1
-    for (int g = 0; g < 2; ++g) {
+    // read D[grp] of this thread's row, write the 16 outputs (split or fp32)
+    auto readout = [&](int grp, uint32_t b, const uint32_t (&lo)[16], bool chain, uint64_t inv2) {
         uint32_t h0[32], h1[32];
-        tmem_ld32(tmem + lane_off + 64 * g, h0);
-        tmem_ld32(tmem + lane_off + 64 * g + 32, h1);
+        tmem_ld32(tmem + lane_off + 64 * grp, h0);
+        tmem_ld32(tmem + lane_off + 64 * grp + 32, h1);
         tmem_wait_ld();
-        const uint32_t b = obase ^ (g ? ogrp : 0u);
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
             const uint64_t y = add2(pk2(__uint_as_float(h0[2 * c]), __uint_as_float(h0[2 * c + 1])),
@@ -196,8 +188,118 @@ __device__ __forceinline__ void tc_gate_f16(float2* tile, uint32_t w_smem, const
             else
                 *reinterpret_cast<float2*>(tb8 + (b ^ lo[c])) = upk2(mul2(y, inv2));
         }
+    };
+#pragma unroll 1
+    for (int g = g0; g < g1; ++g) {
+        const GateDesc& G = gdesc[g];
+        // next operand layout: byte offsets of this gate's roles (the group bit is
+        // the same tile bit in both gates: group grp stays in region grp)
+        const uint4 x0 = *reinterpret_cast<const uint4*>(&G.xu[0]);   // xu[0..7]
+        const uint2 x1 = *reinterpret_cast<const uint2*>(&G.xu[8]);   // xu[8..11]
+        const uint32_t xu[12] = {x0.x & 0xffffu, x0.x >> 16, x0.y & 0xffffu, x0.y >> 16,
+                                 x0.z & 0xffffu, x0.z >> 16, x0.w & 0xffffu, x0.w >> 16,
+                                 x1.x & 0xffffu, x1.x >> 16, x1.y & 0xffffu, x1.y >> 16};
+        uint32_t obase = 0;
+#pragma unroll
+        for (int i = 0; i < 7; ++i)
+            if ((tid >> i) & 1u) obase ^= xu[5 + i];
+        uint32_t lo[16];
+        lo[0] = 0;
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int x = 0; x < (1 << m); ++x) lo[x + (1 << m)] = lo[x] ^ xu[m];
+        if (xu[4] != (uint32_t)kF16GroupBytes) {
+            // the next gate uses another group bit: outputs of either group land in
+            // both regions, so both MMAs finish before any write (no overlap)
+            mbar_wait(mbar, ph[0]);
+            ph[0] ^= 1u;
+            mbar_wait(mbar + 1, ph[1]);
+            ph[1] ^= 1u;
+            fence_after();
+            readout(0, obase, lo, true, 0);
+            readout(1, obase ^ xu[4], lo, true, 0);
+            if (g + 2 < ng) {  // both MMAs of gate g are done: its W buffer takes W(g + 2)
+                const char* src = reinterpret_cast<const char*>(pool + gdesc[g + 2].mat_off);
+                unsigned char* dst = mbuf + (g & 1) * mbuf_bytes;
+                const int chunks = (gdesc[g + 2].k & kGateTC)
+                                       ? (kF16GateBytes >> 4)
+                                       : ((int)sizeof(float2) << (2 * (gdesc[g + 2].k & 0xff))) >> 4;
+                for (int c = (int)tid; c < chunks; c += NT) cp_async16(dst + 16 * c, src + 16 * c);
+                cp_async_commit();
+                cp_async_wait_group1();  // W(g + 1) landed (W(g + 2) may be in flight)
+            } else {
+                cp_async_wait_all();
+            }
+            fence_proxy_async();
+            fence_before();
+            __syncthreads();
+            if (tid == 0) {
+                issue(g + 1, 0);
+                issue(g + 1, 1);
+            }
+            __syncwarp();
+            continue;
+        }
+        // group 0: read D0, write the rows, barrier, then the next gate's group-0
+        // MMAs (issued by thread 0) overlap the group-1 readout
+        QT_MARK(0);
+        mbar_wait(mbar, ph[0]);
+        ph[0] ^= 1u;
+        fence_after();
+        QT_MARK(1);
+        readout(0, obase, lo, true, 0);
+        QT_MARK(2);
+        cp_async_wait_all();  // W(g + 1)
+        fence_proxy_async();
+        fence_before();
+        __syncthreads();
+        if (tid == 0) issue(g + 1, 0);
+        __syncwarp();
+        QT_MARK(3);
+        // group 1 (issued by thread 64)
+        mbar_wait(mbar + 1, ph[1]);
+        ph[1] ^= 1u;
+        fence_after();
+        QT_MARK(4);
+        readout(1, obase ^ xu[4], lo, true, 0);
+        QT_MARK(5);
+        if (g + 2 < ng) {  // both MMAs of gate g are done: its W buffer takes W(g + 2)
+            const char* src = reinterpret_cast<const char*>(pool + gdesc[g + 2].mat_off);
+            unsigned char* dst = mbuf + (g & 1) * mbuf_bytes;
+            const int chunks = (gdesc[g + 2].k & kGateTC) ? (kF16GateBytes >> 4)
+                                                          : ((int)sizeof(float2) << (2 * (gdesc[g + 2].k & 0xff))) >> 4;
+            for (int c = (int)tid; c < chunks; c += NT) cp_async16(dst + 16 * c, src + 16 * c);
+            cp_async_commit();
+        }
+        fence_proxy_async();
+        fence_before();
+        __syncthreads();
+        if (tid == 64) issue(g + 1, 1);
+        __syncwarp();
+        QT_MARK(6);
+#ifdef QT_TIMING
+        if (ts) {
+            for (int i = 0; i < 6; ++i) atomicAdd(timing + tw + i, (unsigned long long)(tm[i + 1] - tm[i]));
+            if (threadIdx.x == 0) atomicAdd(timing + 15, 1ull);
+        }
+#endif
     }
-    fence_before();
+#undef QT_MARK
+    {   // last gate of the run: both groups complete, then the fp32 tile
+        uint32_t lo[16], ogrp, obase;
+        fp32_layout<T>(gdesc[g1], lo, ogrp, obase);
+        mbar_wait(mbar, ph[0]);
+        ph[0] ^= 1u;
+        mbar_wait(mbar + 1, ph[1]);
+        ph[1] ^= 1u;
+        fence_after();
+        const uint64_t inv2 = pk2(run_inv, run_inv);
+#pragma unroll 1
+        for (int grp = 0; grp < 2; ++grp) readout(grp, obase ^ (grp ? ogrp : 0u), lo, false, inv2);
+        fence_before();
+    }
+    return g1;
 }
 
 // Apply one padded 4-qubit gate on tensor cores with 3xTF32 (single-gate runs:
@@ -369,7 +471,7 @@ struct TileCfg {
     static constexpr size_t kGdescOff = kRedOff + 64 * sizeof(double);
     static constexpr size_t kMbarOff = kGdescOff + sizeof(GateDesc) * kMaxPassGates;
     static_assert(!TC || TCK != 4 || tc::gate_bytes(4) == tc::kF16GateBytes, "f16 operand size");
-    static constexpr size_t kBytes = kMbarOff + 16 + 1024;  // + alignment slack
+    static constexpr size_t kBytes = kMbarOff + 16 + 1024;  // 2 mbarriers + alignment slack
 };
 
 template <int T, int R, bool TC, int TCK = 4>
@@ -384,9 +486,23 @@ tile_pass_kernel(const TileArgs A, const int step) {
     constexpr int NA = Cfg::NA;
     constexpr int CL = Cfg::CL;
     constexpr int NH = Cfg::NH;
-    const int slot = A.slots ? A.slots[blockIdx.y] : (int)blockIdx.y;
-    if (step >= A.pass_count[slot]) return;
-    const PassDesc P = A.passes[A.pass_start[slot] + step];
+#ifdef QT_TIMING
+    long long kt[6];
+    kt[0] = clock64();
+#define QT_KMARK(i) kt[i] = clock64()
+#else
+#define QT_KMARK(i)
+#endif
+    // this CTA's pass: one load from the per-step array (executor), else via the slot tables
+    const PassDesc* Pp;
+    if (A.step_passes) {
+        Pp = A.step_passes + blockIdx.y;
+    } else {
+        if (step >= A.pass_count[blockIdx.y]) return;
+        Pp = A.passes + A.pass_start[blockIdx.y] + step;
+    }
+    const PassDesc P = *Pp;
+    const int slot = A.step_passes ? P.slot : (int)blockIdx.y;
 
     extern __shared__ unsigned char smem_raw[];
     // 1024-byte alignment by offsetting smem_raw itself (keeps the pointer in the
@@ -417,11 +533,14 @@ tile_pass_kernel(const TileArgs A, const int step) {
     float2* st = A.state + ((uint64_t)slot << n);
     const int ng = P.gate_count;
 
-    uint32_t tmem = 0, phase = 0;
+    uint32_t tmem = 0;
+    // mbarrier phases: [0] D group 0 (tf32 gates, f16 group 0), [1] D group 1
+    uint32_t ph[2] = {0u, 0u};
     if constexpr (TC) {
         if (ng > 0 && (tid >> 5) == 0) tc::tmem_alloc(&s_tmem, kTmemCols);  // CTAs / SM share 512 columns
         if (tid == 0) {
-            tc::mbar_init(mbar, 1);
+            tc::mbar_init(mbar, 1);        // D of group 0 ready (tcgen05.commit)
+            tc::mbar_init(mbar + 1, 1);    // D of group 1 ready
             tc::fence_mbar_init();
         }
     }
@@ -443,22 +562,12 @@ tile_pass_kernel(const TileArgs A, const int step) {
         tc::fence_after();
         tmem = s_tmem;
     }
-    // warm L2 with the same-slot tile one resident wave ahead (its CTA will load it soon)
-    if (A.prefetch && blockIdx.x + A.prefetch < gridDim.x) {
-        const uint64_t nb = pdep64((uint64_t)(blockIdx.x + A.prefetch), nmask & ~P.tile_mask);
-        for (int h = tid; h < NH; h += NT)
-            asm volatile("prefetch.global.L2 [%0];\n" ::"l"(st + nb + hoff[h]));
-    }
-    // HBM -> shared.  Wide tiles: 16-byte loads of amplitude pairs (thread t owns
-    // pairs p = t + m NT, so lanes cover 8 x 16 B of each 128-byte run), all
-    // issued before the swizzled 8-byte shared stores.  hoff is linear in its
-    // index bits: hoff[(t >> 3) + m NT / 8] = hoff[t >> 3] | hoff[m NT / 8].
-    constexpr bool kWide = (CL == 4) && (NT >= 8) && (NA >= 2) && (NA <= 32);
-    // 8-byte asynchronous copies: the swizzle keeps amplitude pairs adjacent but
-    // not 16-byte aligned.  (Measured at n = 30: register-staged 16-byte loads
-    // 61% of HBM peak vs async 8-byte copies 68%.)
-    // hoff and swz are linear in the index bits: slot L = tid + m NT has global
-    // offset hoff[tid >> CL] + hoff[m NT >> CL] + (tid & (2^CL - 1)) (NT >= 2^CL)
+    QT_KMARK(1);
+    // HBM -> shared: 8-byte asynchronous copies (the swizzle keeps amplitude pairs
+    // adjacent but not 16-byte aligned; register-staged 16-byte loads measured 61%
+    // of HBM peak vs 68% for async copies at n = 30).  hoff and swz are linear in
+    // the index bits: slot L = tid + m NT has global offset hoff[tid >> CL] +
+    // hoff[m NT >> CL] + (tid & (2^CL - 1)) (NT >= 2^CL).
     if constexpr (NT >= (1 << CL)) {
         const float2* gsrc = st + base + hoff[tid >> CL] + ((uint32_t)tid & ((1u << CL) - 1u));
         const uint32_t sb = swz((uint32_t)tid);
@@ -474,42 +583,33 @@ tile_pass_kernel(const TileArgs A, const int step) {
         }
     }
     cp_async_commit();
-    cp_async_wait_all();  // gate descriptors (the tile may still be in flight for other threads)
+    cp_async_wait_all();  // gate descriptors + tile
     __syncthreads();
+    QT_KMARK(2);
     auto mat_bytes = [](const GateDesc& G) -> int {
         return (TC && (G.k & kGateTC)) ? tc::gate_bytes(TCK) : (int)sizeof(float2) * (1 << (2 * (G.k & 0xff)));
     };
-    if (ng > 0) {
-        const int chunks = mat_bytes(gdesc[0]) >> 4;
-        for (int c = tid; c < chunks; c += NT)
-            cp_async16(mbuf + 16 * c, reinterpret_cast<const char*>(A.pool + gdesc[0].mat_off) + 16 * c);
+    // gate matrices: double-buffered, cooperative cp.async (measured faster than
+    // one-thread bulk copies completing on an mbarrier)
+    auto load_w = [&](int g) {
+        unsigned char* dst = mbuf + (g & 1) * Cfg::kMbufBytes;
+        const char* src = reinterpret_cast<const char*>(A.pool + gdesc[g].mat_off);
+        const int chunks = mat_bytes(gdesc[g]) >> 4;
+        for (int c = tid; c < chunks; c += NT) cp_async16(dst + 16 * c, src + 16 * c);
         cp_async_commit();
-    }
-    float run_scale = 1.f, run_inv = 1.f;  // tensor-core run: tile scale (uniform)
+    };
+    if (ng > 0) load_w(0);
     for (int gi = 0; gi < ng; ++gi) {
         const GateDesc& G = gdesc[gi];
         cp_async_wait_all();
-        if constexpr (TC) tc::fence_proxy_async();  // cp.async W / st.shared operand -> tensor-core reads
-        __syncthreads();  // tile writes of the previous gate + this gate's matrix visible
-        if (gi + 1 < ng) {
-            const GateDesc& Gn = gdesc[gi + 1];
-            unsigned char* dst = mbuf + ((gi + 1) & 1) * Cfg::kMbufBytes;
-            const char* src = reinterpret_cast<const char*>(A.pool + Gn.mat_off);
-            if (TC && TCK == 4 && (Gn.k & kGateTC)) {
-                constexpr int kPer = tc::kF16GateBytes / 16 / NT;
-#pragma unroll
-                for (int c = 0; c < kPer; ++c) cp_async16(dst + 16 * (tid + c * NT), src + 16 * (tid + c * NT));
-            } else {
-                const int chunks = mat_bytes(Gn) >> 4;
-                for (int c = tid; c < chunks; c += NT) cp_async16(dst + 16 * c, src + 16 * c);
-            }
-            cp_async_commit();
-        }
+        if constexpr (TC) tc::fence_proxy_async();  // cp.async W / st.shared rows -> tensor-core reads
+        __syncthreads();  // tile writes of the previous gate visible; W buffer (gi + 1) & 1 free
+        if (gi + 1 < ng) load_w(gi + 1);
         unsigned char* mcur = mbuf + (gi & 1) * Cfg::kMbufBytes;
         if constexpr (TC && TCK == 4) {
-            if (G.k & kGateF16) {
-                tc_gate_f16<T>(tile, (uint32_t)__cvta_generic_to_shared(mcur), G, gi + 1 < ng ? &gdesc[gi + 1] : nullptr,
-                               tmem, mbar, phase, run_scale, run_inv, red);
+            if (G.k & kGateF16) {  // run start (runs end before any non-f16 gate)
+                gi = tc_run_f16<T>(tile, mbuf, (uint32_t)Cfg::kMbufBytes, gdesc, gi, ng, A.pool, tmem, mbar, ph, red,
+                                   A.timing);
                 continue;
             }
         }
@@ -525,10 +625,10 @@ tile_pass_kernel(const TileArgs A, const int step) {
             if (G.k & kGateTC) {
                 if constexpr (R == 5 && TCK == 4)
                     apply_tc_gate(tile, (uint32_t)__cvta_generic_to_shared(mcur), swz(tb) << 3, unit, tmem, mbar,
-                                  phase);
+                                  ph[0]);
                 else if constexpr (R == 5 && TCK == 5)
                     apply_tc_gate5(tile, (uint32_t)__cvta_generic_to_shared(mcur), swz(tb) << 3, unit, tmem, mbar,
-                                   phase);
+                                   ph[0]);
             } else if ((G.k & 0xff) == 1) {  // device-chosen conventional operators (q <= 2)
                 apply_fused<1, R>(tile, reinterpret_cast<const float2*>(mcur), swz(tb) << 3, unit);
             } else {
@@ -540,6 +640,7 @@ tile_pass_kernel(const TileArgs A, const int step) {
     }
     cp_async_wait_all();  // a pass without gates still has its tile in flight
     __syncthreads();
+    QT_KMARK(3);
 
     // ---- epilogues (read-only on the tile) ----
     const uint32_t ntiles = gridDim.x;
@@ -667,7 +768,10 @@ tile_pass_kernel(const TileArgs A, const int step) {
         }
     }
 
-    // ---- shared -> HBM ----
+    QT_KMARK(4);
+    // ---- shared -> HBM: 16-byte stores of amplitude pairs (thread t owns pairs
+    // p = t + m NT, lanes cover 8 x 16 B of each 128-byte run) ----
+    constexpr bool kWide = (CL == 4) && (NT >= 8) && (NA >= 2) && (NA <= 32);
     if (P.flags & kPassStore) {
         if constexpr (kWide) {
             float4* gdst = reinterpret_cast<float4*>(st + base + hoff[tid >> 3] + 2 * (tid & 7));
@@ -687,6 +791,14 @@ tile_pass_kernel(const TileArgs A, const int step) {
             }
         }
     }
+    QT_KMARK(5);
+#ifdef QT_TIMING
+    if (A.timing && tid == 0 && (blockIdx.x % 32u) == 7u) {
+        for (int i = 0; i < 5; ++i) atomicAdd(A.timing + 8 + i, (unsigned long long)(kt[i + 1] - kt[i]));
+        atomicAdd(A.timing + 14, 1ull);
+    }
+#endif
+#undef QT_KMARK
     if constexpr (TC) {
         if (ng > 0) {
             tc::fence_before();
@@ -703,6 +815,18 @@ inline size_t tile_pass_smem_bytes_impl(int T, int R, bool tcm, int tck = 4) {
     return 2 * mb + (sizeof(float2) << T) + sizeof(uint64_t) * nh + 64 * sizeof(double) +
            sizeof(GateDesc) * kMaxPassGates + 16 + 1024;
 }
+
+#ifdef QT_TIMING
+// diagnostics build: phase-sum counters shared by every tile-pass launch
+inline unsigned long long* timing_buffer() {
+    static unsigned long long* p = nullptr;
+    if (!p) {
+        cudaMalloc(&p, 16 * sizeof(unsigned long long));
+        cudaMemset(p, 0, 16 * sizeof(unsigned long long));
+    }
+    return p;
+}
+#endif
 
 template <int T, int R, bool TC, int TCK = 4>
 cudaError_t launch_tr(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s) {
@@ -723,6 +847,9 @@ cudaError_t launch_tr(const TileArgs& a, int step, uint32_t ntiles, int nslots, 
     }
     TileArgs b = a;
     b.prefetch = 0;  // measured: L2 prefetch of the next wave's tiles did not help (64% vs 66% of HBM)
+#ifdef QT_TIMING
+    b.timing = timing_buffer();
+#endif
     (void)resident;
     dim3 grid(ntiles, nslots);
     tile_pass_kernel<T, R, TC, TCK><<<grid, Cfg::NT, smem, s>>>(b, step);

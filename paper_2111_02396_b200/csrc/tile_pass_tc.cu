@@ -12,3 +12,9 @@ cudaError_t launch_tile_pass_tc(const TileArgs& a, int tck, int step, uint32_t n
 }
 
 }  // namespace qt
+
+#ifdef QT_TIMING
+extern "C" int qt_timing_read(unsigned long long* host16) {
+    return (int)cudaMemcpy(host16, qt::timing_buffer(), 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+}
+#endif
