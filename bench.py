@@ -295,7 +295,8 @@ def bench_gpu(args):
     else:
         roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": frac_hbm,
                 "traffic": None, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
-                "alu": {"achieved_tflops": achieved_tf, "peak_tflops": fp32_peak_tf, "frac": frac_alu}}
+                "fp32_equivalent": {"achieved_tflops": achieved_tf, "peak_tflops": fp32_peak_tf, "frac": frac_alu,
+                                     "note": "fused-gate flops (P:135) vs the FP32 pipes; context only: the tensor-core K1 runs them on tcgen05"}}
     # traffic: DRAM bytes per launch from the committed ncu --set full capture,
     # scaled to this run's average launch (ratio dram/algorithmic of that capture)
     tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
@@ -305,7 +306,7 @@ def bench_gpu(args):
         roof["traffic_unit"] = "bytes/launch"
         roof["traffic_source"] = tr["source"]
     roof["alg_bytes_per_launch"] = alg_bytes / max(pass_launches, 1)
-    roof["kernel"] = ("tile_pass_kernel<12,5,tensor-core,%d>" % (4 if args.fuse <= 4 else 5)
+    roof["kernel"] = ("tile_pass_kernel<12,%d,tensor-core,%d>" % ((5, 5) if args.fuse > 4 else (5, 4))
                       if args.tensor_cores_on else "tile_pass_kernel<12,4> (CUDA cores)")
     roof["launches_timed"] = int(pass_launches)
     roof["avg_launch_ms"] = pass_ms / max(pass_launches, 1)

@@ -661,14 +661,25 @@ tile_pass_kernel(const TileArgs A, const int step) {
         if (tid == 0) s_last = (atomicAdd(&A.counters[slot], 1) == (int)ntiles - 1);
         __syncthreads();
         if (s_last) {
+            // last CTA of the slot: sum the tile partials with every thread (tiles
+            // strided over threads, then a fixed-order block sum), 8 entries at a time
             __threadfence();
             const int ne = 2 * C.d * C.d;
-            double* fin = red;  // ne <= 32 doubles
-            for (int e = tid; e < ne; e += NT) {
-                double s = 0.0;
-                for (uint32_t t = 0; t < ntiles; ++t)
-                    s += __ldcg(A.rho_part + ((uint64_t)slot * ntiles + t) * A.rho_stride + e);
-                fin[e] = s;
+            double* fin = reinterpret_cast<double*>(gdesc);  // ne <= 32 doubles (gate descriptors are done)
+            const double* part = A.rho_part + (uint64_t)slot * ntiles * A.rho_stride;
+            for (int e0 = 0; e0 < ne; e0 += 8) {
+                double acc[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+                for (uint32_t t = tid; t < ntiles; t += NT)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (e0 + j < ne) acc[j] += __ldcg(part + (uint64_t)t * A.rho_stride + e0 + j);
+                block_sum_n<NT, 8>(acc, red);
+                if (tid == 0)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (e0 + j < ne) fin[e0 + j] = acc[j];
             }
             __syncthreads();
             if (tid == 0) {
