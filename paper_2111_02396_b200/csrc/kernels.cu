@@ -51,24 +51,32 @@ cudaError_t launch_tile_pass(const TileArgs& a, int R, int tck, int step, uint32
 }
 
 // ---------------------------------------------------------------------------
-// K6 fused-matrix materialization (fp64), one CTA per fused gate, thread c
-// builds column c: e_c pushed through the constituents in time order.
+// K6 fused-matrix materialization (fp64), one CTA per fused gate: the D x D
+// product of the constituents (time order) is built in shared memory, one
+// thread per matrix element (r, c) per step: V <- (I (x) C_j) V, i.e.
+// V'[r][c] = sum_a C_j[r_j][a] V[r with its constituent bits := a][c].
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(64)
+constexpr int kMatThreads = 256;
+
+__global__ void __launch_bounds__(kMatThreads)
 materialize_kernel(const FusedDesc* __restrict__ fused, const ConsDesc* __restrict__ cons,
                    const VarDesc* __restrict__ vars, const double2* __restrict__ var_data,
                    float2* __restrict__ pool) {
+    extern __shared__ double2 sm2[];  // two D x D buffers
     const FusedDesc F = fused[blockIdx.x];
     const bool tcm = (F.k & kGateTC) != 0;
-    const int D = 1 << (F.k & 0xff);
-    const int c = threadIdx.x;
-    if (c >= D) return;
-    double2 v[64];
-    for (int i = 0; i < D; ++i) v[i] = make_double2(i == c ? 1.0 : 0.0, 0.0);
+    const int k = F.k & 0xff;
+    const int D = 1 << k;
+    const int DD = D * D;
+    double2* v = sm2;
+    double2* nv = sm2 + DD;
+    for (int e = threadIdx.x; e < DD; e += kMatThreads)
+        v[e] = make_double2((e / D) == (e % D) ? 1.0 : 0.0, 0.0);
+    __syncthreads();
     for (int j = 0; j < F.cons_count; ++j) {
         const ConsDesc C = cons[F.cons_begin + j];
-        const VarDesc V = vars[C.var];
-        const int q = V.nq;
+        const VarDesc Vd = vars[C.var];
+        const int q = Vd.nq;
         const int dq = 1 << q;
         uint32_t qm = 0;
         int pos[6];
@@ -76,42 +84,43 @@ materialize_kernel(const FusedDesc* __restrict__ fused, const ConsDesc* __restri
             pos[m] = (C.pos >> (4 * m)) & 15;
             qm |= 1u << pos[m];
         }
-        const double2* M = var_data + V.off;
-        for (int b0 = 0; b0 < D; ++b0) {
-            if (b0 & qm) continue;
-            double2 in[64];
-            int idx[64];
-            for (int a = 0; a < dq; ++a) {
-                int o = b0;
+        const double2* M = var_data + Vd.off;
+        for (int e = threadIdx.x; e < DD; e += kMatThreads) {
+            const int r = e / D, c = e % D;
+            int rl = 0;
+            for (int m = 0; m < q; ++m) rl |= ((r >> pos[m]) & 1) << m;
+            const int base = r & ~(int)qm;
+            double re = 0.0, im = 0.0;
+            for (int al = 0; al < dq; ++al) {
+                int o = base;
                 for (int m = 0; m < q; ++m)
-                    if ((a >> m) & 1) o |= 1 << pos[m];
-                idx[a] = o;
-                in[a] = v[o];
+                    if ((al >> m) & 1) o |= 1 << pos[m];
+                const double2 u = M[rl * dq + al];
+                const double2 x = v[o * D + c];
+                re += u.x * x.x - u.y * x.y;
+                im += u.x * x.y + u.y * x.x;
             }
-            for (int rr = 0; rr < dq; ++rr) {
-                double re = 0.0, im = 0.0;
-                for (int a = 0; a < dq; ++a) {
-                    const double2 u = M[rr * dq + a];
-                    re += u.x * in[a].x - u.y * in[a].y;
-                    im += u.x * in[a].y + u.y * in[a].x;
-                }
-                v[idx[rr]] = make_double2(re, im);
-            }
+            nv[e] = make_double2(re, im);
         }
+        __syncthreads();
+        double2* t = v;
+        v = nv;
+        nv = t;
     }
+    // element (j, c) of the fused matrix U = v[j * D + c]
     if (!tcm) {
-        for (int rr = 0; rr < D; ++rr) pool[F.mat_off + rr * D + c] = make_float2((float)v[rr].x, (float)v[rr].y);
+        for (int e = threadIdx.x; e < DD; e += kMatThreads)
+            pool[F.mat_off + e] = make_float2((float)v[e].x, (float)v[e].y);
         return;
     }
-    const int k = F.k & 0xff;
     if (k == 4 && (F.k & kGateF16)) {
         // kind::f16 operand B (tc_common.cuh): B[2j + b][4c + q] = hi(blk[q & 1][b]),
         // B[32 + 2j + b][4c + q] = lo(blk[q & 1][b]) for q < 2, 0 for q >= 2, with
         // blk the real 2x2 block of U[j][c] (input component a, output component b).
-        // Column c of U = v.
         __half* B = reinterpret_cast<__half*>(pool + F.mat_off);
-        for (int j = 0; j < D; ++j) {
-            const double ur = v[j].x, ui = v[j].y;
+        for (int e = threadIdx.x; e < DD; e += kMatThreads) {
+            const int jj = e / D, c = e % D;
+            const double ur = v[e].x, ui = v[e].y;
             const double blk[2][2] = {{ur, ui}, {-ui, ur}};
             for (int b = 0; b < 2; ++b)
                 for (int q = 0; q < 4; ++q) {
@@ -119,37 +128,46 @@ materialize_kernel(const FusedDesc* __restrict__ fused, const ConsDesc* __restri
                     const __half h = __double2half(w);
                     const __half l = __double2half(w - (double)__half2float(h));
                     const int kk = 4 * c + q;
-                    B[tc::sw128_offset(2 * j + b, 2 * kk) >> 1] = h;
-                    B[tc::sw128_offset(32 + 2 * j + b, 2 * kk) >> 1] = q < 2 ? l : __float2half(0.f);
+                    B[tc::sw128_offset(2 * jj + b, 2 * kk) >> 1] = h;
+                    B[tc::sw128_offset(32 + 2 * jj + b, 2 * kk) >> 1] = q < 2 ? l : __float2half(0.f);
                 }
         }
         return;
     }
-    // 3xTF32 operand W (tc_common.cuh; 5 qubits, and 4-qubit single-gate runs): W[2c + a][2j + b] = real 2x2 block of
-    // U[j][c], stored K-major swizzled as hi then lo tf32 parts.  Column c of U = v.
+    // 3xTF32 operand W (tc_common.cuh; 5 qubits): W[2c + a][2j + b] = real 2x2
+    // block of U[j][c], stored K-major swizzled as hi then lo tf32 parts
     uint32_t* W = reinterpret_cast<uint32_t*>(pool + F.mat_off);
     const uint32_t part = (uint32_t)tc::w_part_bytes(k) >> 2;
-    for (int j = 0; j < D; ++j) {
-        const double ur = v[j].x, ui = v[j].y;
+    for (int e = threadIdx.x; e < DD; e += kMatThreads) {
+        const int jj = e / D, c = e % D;
+        const double ur = v[e].x, ui = v[e].y;
         const double blk[2][2] = {{ur, ui}, {-ui, ur}};
-        for (int a = 0; a < 2; ++a)
+        for (int a2 = 0; a2 < 2; ++a2)
             for (int b = 0; b < 2; ++b) {
-                const float w = (float)blk[a][b];
+                const float w = (float)blk[a2][b];
                 const uint32_t h = tc::tf32_rna(w);
                 const uint32_t l = tc::tf32_rna(w - __uint_as_float(h));
-                const uint32_t off = tc::w_offset_bytes_k(k, 2 * j + b, 2 * c + a) >> 2;
+                const uint32_t off = tc::w_offset_bytes_k(k, 2 * jj + b, 2 * c + a2) >> 2;
                 W[off] = h;
                 W[part + off] = l;
             }
     }
 }
 
-cudaError_t launch_materialize(const FusedDesc* fused, int n_fused, const ConsDesc* cons,
-                               const VarDesc* vars, const double* var_data, float2* pool,
-                               cudaStream_t s) {
+cudaError_t launch_materialize(const FusedDesc* fused, int n_fused, int max_k, const ConsDesc* cons,
+                               const VarDesc* vars, const double* var_data, float2* pool, cudaStream_t s) {
     if (n_fused <= 0) return cudaSuccess;
-    materialize_kernel<<<n_fused, 64, 0, s>>>(fused, cons, vars,
-                                             reinterpret_cast<const double2*>(var_data), pool);
+    const int kk = max_k < 1 ? 1 : (max_k > 6 ? 6 : max_k);
+    const size_t smem = 2 * sizeof(double2) * ((size_t)1 << (2 * kk));
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(materialize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(2 * sizeof(double2) * 64 * 64));
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    materialize_kernel<<<n_fused, kMatThreads, smem, s>>>(fused, cons, vars, reinterpret_cast<const double2*>(var_data),
+                                                           pool);
     return cudaGetLastError();
 }
 

@@ -45,7 +45,8 @@ size_t tile_pass_smem_bytes(int T, int R, int tck);
 cudaError_t launch_tile_pass(const TileArgs& a, int R, int tck, int step, uint32_t ntiles, int nslots,
                              cudaStream_t s);
 
-cudaError_t launch_materialize(const FusedDesc* fused, int n_fused, const ConsDesc* cons,
+// max_k: largest fused-gate arity of the call (threads per gate = 2^max_k)
+cudaError_t launch_materialize(const FusedDesc* fused, int n_fused, int max_k, const ConsDesc* cons,
                                const VarDesc* vars, const double* var_data, float2* pool,
                                cudaStream_t s);
 

@@ -386,7 +386,8 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
     // |0...0> in every slot
     QT_CK(launch_init_states(state, n, nslots, s));
     uint64_t launches = 1;
-    QT_CK(launch_materialize(B.fused.as<FusedDesc>(), (int)nf, B.cons.as<ConsDesc>(), ctx->vars.as<VarDesc>(),
+    QT_CK(launch_materialize(B.fused.as<FusedDesc>(), (int)nf, P.tc ? P.tc_k : P.R, B.cons.as<ConsDesc>(),
+                             ctx->vars.as<VarDesc>(),
                              ctx->var_data.as<double>(), B.pool.as<float2>(), s));
     launches += nf > 0;
     TileArgs A;
@@ -715,7 +716,7 @@ static qt_status run_single(qt_ctx ctx, qt_plan plan, float2* state, const ObsGr
     QT_CK(B.records.ensure(16));
     QT_CK(cudaMemsetAsync(B.status.p, 0, sizeof(int32_t), s));
     QT_CK(cudaMemsetAsync(B.counters.p, 0, sizeof(int32_t), s));
-    QT_CK(launch_materialize(B.fused.as<FusedDesc>(), (int)pg.fused.size(), B.cons.as<ConsDesc>(),
+    QT_CK(launch_materialize(B.fused.as<FusedDesc>(), (int)pg.fused.size(), P.tc ? P.tc_k : P.R, B.cons.as<ConsDesc>(),
                              ctx->vars.as<VarDesc>(), ctx->var_data.as<double>(), B.pool.as<float2>(), s));
     TileArgs A{};
     A.state = state;
