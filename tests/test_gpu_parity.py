@@ -227,3 +227,70 @@ def test_config2_sample_of_trajectories(ctx):
                                shots=1, observables=c.observables)
     torch.cuda.synchronize()
     compare(ref, out, state)
+
+
+# ---------------------------------------------------------------------------
+# K1 f16 tensor-core runs: the tile scale (DESIGN R11) under norm growth,
+# tiny amplitudes and all-zero tiles; chains of 4-qubit operators applied with
+# qt_apply_plan vs the oracle's Alg. 1 one operator at a time.
+# ---------------------------------------------------------------------------
+def _chain(rng, n_ops, low=12):
+    ops = []
+    prev = None
+    for _ in range(n_ops):
+        while True:
+            qs = sorted(int(x) for x in rng.choice(low, 4, replace=False))
+            if qs != prev:
+                break
+        prev = qs
+        ops.append((qs, workloads.haar_unitary(rng, 16)))
+    return ops
+
+
+def _apply_chain(ctx, psi, ops, n):
+    c = qtraj.Circuit(n)
+    for m, (qs, M) in enumerate(ops):
+        c.add_matrix(m, qs, M)
+    plan = qtraj.Plan(c, max_fused=4)
+    d = to_dev(psi)
+    ctx.apply_plan(plan, d)
+    ref = psi.copy()
+    for qs, M in ops:
+        ref = oracle.apply_gate(ref, qs, M)
+    return d.cpu().numpy().astype(np.complex128), ref
+
+
+@pytest.mark.parametrize("scale", [1.0, 3.0, 40.0])
+def test_tc_run_norm_growth(ctx, scale):
+    """Non-unitary operators (qt_add_matrix, as distributed mode's 1/sqrt(p)
+    picks) grow the tile norm by up to scale^4: runs split and widen their
+    scale headroom (2^shift) instead of overflowing the f16 operands."""
+    n = 14
+    rng = np.random.default_rng(7)
+    ops = _chain(rng, 12)
+    ops = [(qs, M * (scale if i % 3 == 0 else 1.0)) for i, (qs, M) in enumerate(ops)]
+    got, ref = _apply_chain(ctx, rand_state(rng, n), ops, n)
+    assert np.all(np.isfinite(got))
+    assert rel_l2(got, ref) < AMP_TOL, rel_l2(got, ref)
+
+
+@pytest.mark.parametrize("amp", [1e-25, 1e-3, 1e3])
+def test_tc_run_amplitude_range(ctx, amp):
+    """The power-of-two tile scale keeps 22 significant bits whatever the
+    amplitude magnitude (unnormalised states, tiny per-rank norms)."""
+    n = 14
+    rng = np.random.default_rng(11)
+    got, ref = _apply_chain(ctx, rand_state(rng, n) * amp, _chain(rng, 10), n)
+    assert rel_l2(got, ref) < AMP_TOL, rel_l2(got, ref)
+
+
+def test_tc_run_zero_tiles(ctx):
+    """Tiles that are entirely zero (max component 0) stay exactly zero."""
+    n = 14
+    rng = np.random.default_rng(12)
+    psi = rand_state(rng, n)
+    psi[np.arange(2 ** n) & (1 << 13) != 0] = 0  # qubit 13 (outside every tile of the chain) in |0>
+    psi /= np.linalg.norm(psi)
+    got, ref = _apply_chain(ctx, psi, _chain(rng, 8), n)
+    assert np.all(got[np.arange(2 ** n) & (1 << 13) != 0] == 0)
+    assert rel_l2(got, ref) < AMP_TOL, rel_l2(got, ref)
