@@ -156,6 +156,14 @@ class Circuit:
         m = _cplx(M)
         _check(lib().qt_add_matrix(self.h, moment, len(q), _iptr(q), _dptr(m)))
 
+    def add_measurement(self, moment: int, qubits: Sequence[int]) -> None:
+        """Mid-circuit computational-basis measurement (one keyed projector channel per
+        qubit: always the conventional branch of Alg. 2; records = outcomes)."""
+        P0 = np.array([[1, 0], [0, 0]], dtype=np.complex128)
+        P1 = np.array([[0, 0], [0, 1]], dtype=np.complex128)
+        for q in qubits:
+            self.add_channel(moment, [q], [P0, P1], True)
+
     def add_channel(self, moment: int, qubits: Sequence[int], kraus: Iterable, record: bool = True) -> None:
         q = np.asarray(qubits, np.int32)
         ks = list(kraus)

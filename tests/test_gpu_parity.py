@@ -294,3 +294,54 @@ def test_tc_run_zero_tiles(ctx):
     got, ref = _apply_chain(ctx, psi, _chain(rng, 8), n)
     assert np.all(got[np.arange(2 ** n) & (1 << 13) != 0] == 0)
     assert rel_l2(got, ref) < AMP_TOL, rel_l2(got, ref)
+
+
+# ---------------------------------------------------------------------------
+# NEXT-3: mid-circuit measurements (keyed projector channels, always the
+# conventional branch) -- identical outcomes, samples and states
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n", [5, 14])
+def test_mid_circuit_measurement_parity(ctx, n):
+    rng = np.random.default_rng(40 + n)
+    c = workloads.random_circuit(n, depth=6, seed=40 + n, max_arity=2, noise="depol")
+    moms = []
+    for i, m in enumerate(c.moments):
+        moms.append(m)
+        if i % 3 == 2:
+            moms.append([workloads.measurement(int(q)) for q in rng.choice(n, 2, replace=False)])
+    c.moments = moms
+    ref, out, state = run_both(ctx, c, seed=123, T=24, shots=2)
+    assert compare(ref, out, state) == 0
+
+
+# ---------------------------------------------------------------------------
+# C4 (32 qubits on one GPU, SURVEY 8(c) pins): no oracle state fits, so a
+# mirror circuit (C then C^dagger) must return |0...0>
+# ---------------------------------------------------------------------------
+def test_mirror_circuit_32_qubits(ctx):
+    n = 32
+    if torch.cuda.get_device_properties(0).total_memory < (40 << 30):
+        pytest.skip("needs a 32 GiB state")
+    rng = np.random.default_rng(32)
+    fwd = []
+    for layer in range(6):
+        qs = rng.permutation(n)
+        for i in range(0, n - 1, 2):
+            fwd.append(((int(qs[i]), int(qs[i + 1])), workloads.haar_unitary(rng, 4)))
+    c = qtraj.Circuit(n)
+    m = 0
+    for qs, U in fwd:
+        c.add_gate(m, list(qs), U)
+        m += 1
+    for qs, U in reversed(fwd):
+        c.add_gate(m, list(qs), U.conj().T)
+        m += 1
+    plan = qtraj.Plan(c, max_fused=4)
+    state = torch.zeros(1 << n, dtype=torch.complex64, device="cuda")
+    out = ctx.run_trajectories(plan, state, seed=1, traj_count=1, batch=1, shots=8, observables=["Z" * 4])
+    torch.cuda.synchronize()
+    a0 = state[0].item()
+    assert abs(abs(a0) - 1.0) < 1e-4, a0
+    assert np.all(out["bits"] == 0)
+    del state
+    torch.cuda.empty_cache()

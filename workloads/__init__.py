@@ -29,7 +29,7 @@ from . import channels
 __all__ = [
     "Gate", "Channel", "Circuit", "flatten", "gates", "channels",
     "ghz4_depolarized", "sycamore_grid_qcs", "low_noise_grid", "random_circuit",
-    "circuit_seed", "trajectory_seed", "haar_unitary",
+    "circuit_seed", "trajectory_seed", "haar_unitary", "measurement", "circuit_to_json", "circuit_from_json",
 ]
 
 
@@ -118,6 +118,68 @@ def flatten(c: Circuit):
         mat_off=np.asarray(mat_off, np.int64),
         mats=np.ascontiguousarray(mats.view(np.float64)),
     )
+
+
+def measurement(qubit: int) -> Channel:
+    """Mid-circuit computational-basis measurement of one qubit as a keyed channel
+    (projectors; the record is the outcome, the state collapses, A12)."""
+    from .channels import measure
+    return Channel((int(qubit),), measure(), name="measure", record=True)
+
+
+def _mat_to_json(m):
+    m = np.asarray(m, dtype=np.complex128)
+    return {"re": m.real.tolist(), "im": m.imag.tolist()}
+
+
+def _mat_from_json(d):
+    return np.asarray(d["re"], dtype=np.float64) + 1j * np.asarray(d["im"], dtype=np.float64)
+
+
+def circuit_to_json(c: Circuit) -> str:
+    """Circuit file format (JSON): moments of gates ({"gate": name, "qubits", "matrix"})
+    and channels ({"channel": name, "qubits", "kraus": [...], "record"}), matrices in
+    Kronecker order of the listed qubits as {"re": rows, "im": rows}; optional
+    readout p00 / p11 and observables (Pauli strings, char q = qubit q)."""
+    import json
+    moms = []
+    for m in c.moments:
+        ops = []
+        for op in m:
+            if isinstance(op, Gate):
+                ops.append({"gate": op.name, "qubits": [int(q) for q in op.qubits], "matrix": _mat_to_json(op.matrix)})
+            else:
+                ops.append({"channel": op.name, "qubits": [int(q) for q in op.qubits],
+                            "kraus": [_mat_to_json(k) for k in op.kraus], "record": bool(op.record)})
+        moms.append(ops)
+    d = {"format": "qtraj-circuit-1", "n_qubits": int(c.n_qubits), "moments": moms,
+         "observables": list(c.observables)}
+    if c.p00 is not None:
+        d["p00"] = np.asarray(c.p00, np.float64).tolist()
+    if c.p11 is not None:
+        d["p11"] = np.asarray(c.p11, np.float64).tolist()
+    return json.dumps(d)
+
+
+def circuit_from_json(text: str) -> Circuit:
+    import json
+    d = json.loads(text)
+    if d.get("format") != "qtraj-circuit-1":
+        raise ValueError("not a qtraj-circuit-1 document")
+    moms = []
+    for m in d["moments"]:
+        ops = []
+        for op in m:
+            if "gate" in op:
+                ops.append(Gate(tuple(op["qubits"]), _mat_from_json(op["matrix"]), name=op["gate"]))
+            else:
+                ops.append(Channel(tuple(op["qubits"]), [_mat_from_json(k) for k in op["kraus"]],
+                                   name=op["channel"], record=bool(op.get("record", True))))
+        moms.append(ops)
+    return Circuit(n_qubits=int(d["n_qubits"]), moments=moms,
+                   p00=np.asarray(d["p00"]) if "p00" in d else None,
+                   p11=np.asarray(d["p11"]) if "p11" in d else None,
+                   observables=list(d.get("observables", [])))
 
 
 def haar_unitary(rng: np.random.Generator, d: int) -> np.ndarray:

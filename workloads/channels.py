@@ -14,6 +14,11 @@ The Kraus list ORDER is data: both sides read the same uploaded list
   amplitude_damp(g): {diag(1, sqrt(1-g)), [[0, sqrt g],[0,0]]}
   phase_damp(g):     {diag(1, sqrt(1-g)), diag(0, sqrt g)}
   bit_flip(p):       {sqrt(1-p) I, sqrt(p) X}
+  measure():         {|0><0|, |1><1|}: a computational-basis measurement as a
+                   channel (P:102 keyed channels): sigma_min of
+                   a projector is 0, so s = 0 and Alg. 2 always takes the
+                   conventional branch -- p_i = <psi|P_i|psi>, collapse
+                   psi <- P_i psi / sqrt(p_i), the record is the outcome i.
 """
 import numpy as np
 
@@ -60,3 +65,7 @@ def phase_damp(g):
 def bit_flip(p):
     I, X, _, _ = paulis()
     return [np.sqrt(1 - p) * I, np.sqrt(p) * X]
+
+
+def measure():
+    return [np.array([[1, 0], [0, 0]], dtype=np.complex128), np.array([[0, 0], [0, 1]], dtype=np.complex128)]
