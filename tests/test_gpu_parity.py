@@ -345,3 +345,16 @@ def test_mirror_circuit_32_qubits(ctx):
     assert np.all(out["bits"] == 0)
     del state
     torch.cuda.empty_cache()
+
+
+def test_calibrated_qcs_noise_model_parity(ctx):
+    """NEXT-2: a circuit with the calibrated approximate QCS noise model
+    (workloads/noise_model.py: Z-phase + fSim coherent errors, depolarizing
+    remainder of the XEB budget, decay from T1 / eps_inc, readout)."""
+    from workloads import noise_model as nm
+    c = workloads.sycamore_grid_qcs(rows=3, cols=4, cycles=4, config=2, noise=False)
+    pairs = sorted({tuple(op.qubits) for op in c.ops() if len(op.qubits) == 2})
+    noisy = nm.synthetic_calibration(c.n_qubits, pairs, seed=8).noisy(c)
+    noisy.observables = ["Z" + "I" * (c.n_qubits - 1), "I" * (c.n_qubits - 1) + "Z"]
+    ref, out, state = run_both(ctx, noisy, seed=77, T=32)
+    assert compare(ref, out, state) == 0
