@@ -93,6 +93,7 @@ struct BatchBufs {
         bits, obs_out, status, counters, rho_part, blocksum, obs_part, slot_list;
     HostBuf h_blob, h_out;
     cudaEvent_t done = nullptr;
+    cudaEvent_t prepared = nullptr;  // uploads + materialization of this batch (prep stream)
     bool inflight = false;
     // host-side bookkeeping of the batch in flight
     int nslots = 0;
@@ -107,6 +108,8 @@ struct BatchBufs {
         h_out.release();
         if (done) cudaEventDestroy(done);
         done = nullptr;
+        if (prepared) cudaEventDestroy(prepared);
+        prepared = nullptr;
     }
 };
 
@@ -115,6 +118,10 @@ struct BatchBufs {
 struct qt_ctx_s {
     int device = 0;
     cudaStream_t stream = nullptr;
+    // uploads + fused-matrix materialization of the next batch overlap the
+    // current batch's passes on this internal stream (ordered by events)
+    cudaStream_t prep = nullptr;
+    cudaEvent_t tables_ready = nullptr;
     BatchBufs bb[2];
     DevBuf vars, var_data, chans, chan_data, obs, p00, p11;
     std::vector<cudaEvent_t> prof_ev;
@@ -365,9 +372,11 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
     QT_CK(B.obs_part.ensure(sizeof(double) * (size_t)nslots * ntiles * std::max(n_obs, 1)));
     QT_CK(B.obs_out.ensure(sizeof(double) * (size_t)nslots * std::max(n_obs, 1)));
     QT_CK(B.bits.ensure(sizeof(uint64_t) * (size_t)nslots * std::max(shots, 1)));
-    // one contiguous H2D per region
+    // one contiguous H2D per region, on the prep stream (the previous user of
+    // these buffers finished: finish_batch waited on B.done)
+    cudaStream_t ps = ctx->prep;
     auto h2d = [&](DevBuf& d, size_t off, size_t bytes) -> qt_status {
-        if (bytes) QT_CK(cudaMemcpyAsync(d.p, hb + off, bytes, cudaMemcpyHostToDevice, s));
+        if (bytes) QT_CK(cudaMemcpyAsync(d.p, hb + off, bytes, cudaMemcpyHostToDevice, ps));
         return QT_OK;
     };
     qt_status e;
@@ -381,15 +390,17 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
     if ((e = h2d(B.records, L.records, sizeof(int32_t) * (size_t)nslots * P.n_recorded)) != QT_OK) return e;
     if ((e = h2d(B.traj_ids, L.traj_ids, sizeof(uint64_t) * nslots)) != QT_OK) return e;
     if ((e = h2d(B.slot_list, L.slot_list, sizeof(PassDesc) * step_off[maxp])) != QT_OK) return e;
-    QT_CK(cudaMemsetAsync(B.status.p, 0, sizeof(int32_t) * nslots, s));
-    QT_CK(cudaMemsetAsync(B.counters.p, 0, sizeof(int32_t) * nslots, s));
-    // |0...0> in every slot
-    QT_CK(launch_init_states(state, n, nslots, s));
-    uint64_t launches = 1;
+    QT_CK(cudaMemsetAsync(B.status.p, 0, sizeof(int32_t) * nslots, ps));
+    QT_CK(cudaMemsetAsync(B.counters.p, 0, sizeof(int32_t) * nslots, ps));
     QT_CK(launch_materialize(B.fused.as<FusedDesc>(), (int)nf, P.tc ? P.tc_k : P.R, B.cons.as<ConsDesc>(),
                              ctx->vars.as<VarDesc>(),
-                             ctx->var_data.as<double>(), B.pool.as<float2>(), s));
-    launches += nf > 0;
+                             ctx->var_data.as<double>(), B.pool.as<float2>(), ps));
+    if (!B.prepared) QT_CK(cudaEventCreateWithFlags(&B.prepared, cudaEventDisableTiming));
+    QT_CK(cudaEventRecord(B.prepared, ps));
+    QT_CK(cudaStreamWaitEvent(s, B.prepared, 0));
+    // |0...0> in every slot (the shared state buffer: stream-ordered after the previous batch)
+    QT_CK(launch_init_states(state, n, nslots, s));
+    uint64_t launches = 1 + (nf > 0);
     TileArgs A;
     A.state = state;
     A.n = n;
@@ -536,6 +547,8 @@ qt_status qt_ctx_create(int device, void* cuda_stream, qt_ctx* out) {
     if (!c) return fail(QT_EOOM, "host allocation failed");
     c->device = device;
     c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+    QT_CK(cudaStreamCreateWithFlags(&c->prep, cudaStreamNonBlocking));
+    QT_CK(cudaEventCreateWithFlags(&c->tables_ready, cudaEventDisableTiming));
     *out = c;
     return QT_OK;
 }
@@ -554,6 +567,11 @@ void qt_ctx_destroy(qt_ctx ctx) {
     for (DevBuf* d : {&ctx->vars, &ctx->var_data, &ctx->chans, &ctx->chan_data, &ctx->obs, &ctx->p00, &ctx->p11})
         d->release();
     for (auto ev : ctx->prof_ev) cudaEventDestroy(ev);
+    if (ctx->prep) {
+        cudaStreamSynchronize(ctx->prep);
+        cudaStreamDestroy(ctx->prep);
+    }
+    if (ctx->tables_ready) cudaEventDestroy(ctx->tables_ready);
     delete ctx;
 }
 
@@ -589,6 +607,8 @@ qt_status qt_run_trajectories(qt_ctx ctx, qt_plan plan, const qt_run_opts* opts,
     QT_CK(cudaEventCreate(&t1));
     QT_CK(cudaEventRecord(t0, s));
     if ((e = upload_plan_tables(ctx, P, obs_table)) != QT_OK) return e;
+    QT_CK(cudaEventRecord(ctx->tables_ready, s));  // materialization (prep stream) reads the tables
+    QT_CK(cudaStreamWaitEvent(ctx->prep, ctx->tables_ready, 0));
     st.h2d_bytes += sizeof(VarDesc) * P.var_desc.size() + sizeof(double) * P.var_data.size() +
                     sizeof(ChanDesc) * P.chans.size() + sizeof(double) * P.chan_data.size() +
                     sizeof(ObsDesc) * obs_table.size() + sizeof(double) * (P.p00.size() + P.p11.size());
