@@ -15,11 +15,12 @@ c = workloads.sycamore_grid_qcs(config=2)
 ctx = qtraj.Context(0)
 plan = qtraj.Plan(qtraj.Circuit.from_description(c), max_fused=4)
 state = torch.empty(128 << 20, dtype=torch.complex64, device="cuda")
-for i in range(3):
+for i in range(3 if @C2@ else 0):
     out = ctx.run_trajectories(plan, state, seed=workloads.trajectory_seed(2), traj_count=1024, batch=128, shots=1,
                                observables=c.observables, profile=True)
-st = out["stats"]
-print(@LIB@, "C2 1024 traj: pass_kernel_ms %.1f device_ms %.1f" % (st["pass_kernel_ms"], st["device_ms"]), flush=True)
+if @C2@:
+    st = out["stats"]
+    print(@LIB@, "C2 1024 traj: pass_kernel_ms %.1f device_ms %.1f" % (st["pass_kernel_ms"], st["device_ms"]), flush=True)
 del state; torch.cuda.empty_cache()
 if @CHAIN@:
     import numpy as np
@@ -51,5 +52,5 @@ if @SWEEP@:
 sweep = "--sweep" in sys.argv
 chain = "--chain" in sys.argv
 for lib in [a for a in sys.argv[1:] if not a.startswith("--")]:
-    code = CODE.replace("@ROOT@", repr(ROOT)).replace("@LIB@", repr(lib)).replace("@SWEEP@", str(sweep)).replace("@CHAIN@", str(chain))
+    code = CODE.replace("@ROOT@", repr(ROOT)).replace("@LIB@", repr(lib)).replace("@SWEEP@", str(sweep)).replace("@CHAIN@", str(chain)).replace("@C2@", str("--no-c2" not in sys.argv))
     subprocess.run([sys.executable, "-c", code], cwd=ROOT)
