@@ -127,7 +127,8 @@ typedef struct {
     int tile_bits;    /* qubits held per CTA tile; 0 = auto (12, or n if n < 12) */
     int low_bits;     /* lowest qubits always in a tile (coalescing); 0 = auto (4) */
     int one_gate_per_pass; /* 1 = every fused gate is its own HBM pass (the paper's GPU scheme) */
-    int tensor_cores;      /* 0 = auto (on when n >= 12 and f <= 4), 1 = on (QT_EINVAL if unsupported),
+    int tensor_cores;      /* 0 = auto (on when n >= 12; fused gates padded to max(f, 4) qubits),
+                              1 = on (QT_EINVAL if unsupported),
                               -1 = off: fused gates on FP32 CUDA cores */
 } qt_fuse_opts;
 qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out);

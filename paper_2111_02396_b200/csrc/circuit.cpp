@@ -401,19 +401,20 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
     P.one_gate = o.one_gate_per_pass != 0;
     // tensor cores: every fused gate padded to 4 qubits (f <= 4), T = 12, 128-thread CTAs
     // whose CUDA-core gates use R = 5
-    const bool tc_ok = (P.T == 12 && f <= 5 && max_arity <= f);
+    const bool tc_ok = (P.T == 12 && max_arity <= f);
     if (o.tensor_cores > 0 && !tc_ok) {
         delete hp;
-        return fail(QT_EINVAL, "tensor_cores needs n >= 12, max_fused <= 5 and gates of <= max_fused qubits");
+        return fail(QT_EINVAL, "tensor_cores needs n >= 12 and gates of <= max_fused qubits");
     }
     P.tc = o.tensor_cores >= 0 && tc_ok;
     if (P.tc) {
         // 128-thread CTAs: f <= 4 -> gates padded to 4 qubits (two 16-amplitude
         // subvectors per thread, 4 CTAs / SM); f = 5 -> padded to 5 qubits (one
-        // 32-amplitude subvector per thread, 2 CTAs / SM)
+        // 32-amplitude subvector per thread, 3 CTAs / SM); f = 6 -> padded to 6
+        // qubits (half a 64-amplitude subvector per thread, 2 CTAs / SM)
         P.R = 5;
         P.f = f;
-        P.tc_k = f <= 4 ? 4 : 5;
+        P.tc_k = f <= 4 ? 4 : f;
     }
     // canonical order: moment ascending, then call order (stable)
     std::vector<const HostOp*> order;

@@ -61,6 +61,10 @@ constexpr int32_t kGateTC = 0x100;
 constexpr int32_t kGateRunStart = 0x200;  // first gate of a tensor-core run
 constexpr int32_t kGateF16 = 0x400;       // 4-qubit gate of a run of >= 2: f16 operands (else 3xTF32)
 constexpr int kGateShiftBit = 16;         // bits 16..23: run scale headroom (log2)
+// Pool bytes of a tensor-core gate operand padded to k qubits (tc_common.cuh
+// gate_bytes): 4 -> f16 B or tf32 hi/lo W (8 KB), 5 -> f16 hi/lo B (16 KB),
+// 6 -> f16 hi/lo B in two K-chunks of 256 rows (64 KB).
+constexpr int tc_gate_bytes(int k) { return k <= 4 ? 8192 : (k == 5 ? 16384 : 65536); }
 
 // A conventional channel occurrence (Alg. 2 lines 12-21).
 struct EventDesc {

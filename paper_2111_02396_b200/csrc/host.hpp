@@ -66,7 +66,7 @@ struct Plan {
     int R = 4;          // register bits (2^R amplitudes / thread)
     bool one_gate = false;
     bool tc = false;    // fused gates padded to tc_k qubits and applied on tcgen05 tensor cores
-    int tc_k = 4;       // 4 (f <= 4) or 5 (f = 5)
+    int tc_k = 4;       // 4 (f <= 4), 5 (f = 5) or 6 (f = 6)
     std::vector<PlanOp> ops;
     std::vector<Variant> vars;
     std::vector<VarDesc> var_desc;

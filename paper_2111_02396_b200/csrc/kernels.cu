@@ -42,7 +42,7 @@ cudaError_t launch_tile_pass(const TileArgs& a, int R, int tck, int step, uint32
                              cudaStream_t s) {
     // Instantiated (T, R): (12, 4), (12, 5), (12, 6) and (T, min(T, 4)) for
     // T = 1..11 (the whole state of n < 12 qubits in one CTA); tensor cores
-    // (tck = 4 or 5 qubits per padded gate): (12, 5).
+    // (tck = 4, 5 or 6 qubits per padded gate): (12, 5).
     if (tck) return a.T == 12 && R == 5 ? launch_tile_pass_tc(a, tck, step, ntiles, nslots, s) : cudaErrorInvalidValue;
     if (a.T == 12 && R == 6) return launch_tile_pass_r6(a, step, ntiles, nslots, s);
     if (a.T == 12 && R == 5) return launch_tile_pass_r5(a, step, ntiles, nslots, s);
@@ -134,8 +134,27 @@ materialize_kernel(const FusedDesc* __restrict__ fused, const ConsDesc* __restri
         }
         return;
     }
-    // 3xTF32 operand W (tc_common.cuh; 5 qubits): W[2c + a][2j + b] = real 2x2
-    // block of U[j][c], stored K-major swizzled as hi then lo tf32 parts
+    if (k >= 5) {
+        // wide f16 operand B (tc_common.cuh): B[2j + b][2c + a] = blk[a][b] of
+        // U[j][c], hi part and lo (remainder) part
+        __half* B = reinterpret_cast<__half*>(pool + F.mat_off);
+        for (int e = threadIdx.x; e < DD; e += kMatThreads) {
+            const int jj = e / D, c = e % D;
+            const double ur = v[e].x, ui = v[e].y;
+            const double blk[2][2] = {{ur, ui}, {-ui, ur}};
+            for (int a2 = 0; a2 < 2; ++a2)
+                for (int b = 0; b < 2; ++b) {
+                    const double w = blk[a2][b];
+                    const __half h = __double2half(w);
+                    const __half l = __double2half(w - (double)__half2float(h));
+                    B[tc::wide_b_offset(k, 0, 2 * jj + b, 2 * c + a2) >> 1] = h;
+                    B[tc::wide_b_offset(k, 1, 2 * jj + b, 2 * c + a2) >> 1] = l;
+                }
+        }
+        return;
+    }
+    // 3xTF32 operand W (tc_common.cuh; single 4-qubit gates): W[2c + a][2j + b] =
+    // real 2x2 block of U[j][c], stored K-major swizzled as hi then lo tf32 parts
     uint32_t* W = reinterpret_cast<uint32_t*>(pool + F.mat_off);
     const uint32_t part = (uint32_t)tc::w_part_bytes(k) >> 2;
     for (int e = threadIdx.x; e < DD; e += kMatThreads) {

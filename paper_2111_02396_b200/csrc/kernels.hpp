@@ -41,7 +41,7 @@ constexpr int kMaxR = 6;
 constexpr int kMaxT = 12;
 
 size_t tile_pass_smem_bytes(int T, int R, int tck);
-// tck: 0 = CUDA-core fused gates; 4 / 5 = tensor-core gates padded to tck qubits.
+// tck: 0 = CUDA-core fused gates; 4 / 5 / 6 = tensor-core gates padded to tck qubits.
 cudaError_t launch_tile_pass(const TileArgs& a, int R, int tck, int step, uint32_t ntiles, int nslots,
                              cudaStream_t s);
 

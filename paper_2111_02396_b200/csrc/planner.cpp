@@ -496,6 +496,14 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
         size_t remaining = fg.size();
         const bool last_seg = (si + 1 == segs.size());
         std::vector<size_t> seg_pass_idx;
+        // tensor cores: a fused gate is padded to tc_k qubits with the lowest
+        // qubits it does not touch, which must lie in the tile too
+        auto padded = [&](const FusedGate& g) {
+            uint64_t pm = g.mask;
+            if (P.tc && g.special_event < 0)
+                for (int q = 0; q < n && popc(pm) < P.tc_k; ++q) pm |= 1ull << q;
+            return pm;
+        };
         while (remaining > 0) {
             uint64_t S = lowS;
             uint64_t blocked = 0;
@@ -504,9 +512,10 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
                 if (taken[i]) continue;
                 const uint64_t gm = fg[i].mask;
                 if (gm & blocked) { blocked |= gm; continue; }
-                if (popc(S | gm) <= T && (!P.one_gate || chosen.empty()) &&
+                const uint64_t gp = padded(fg[i]);
+                if (popc(S | gp) <= T && (!P.one_gate || chosen.empty()) &&
                     (int)chosen.size() < kMaxPassGates) {
-                    S |= gm;
+                    S |= gp;
                     chosen.push_back((int)i);
                 } else {
                     blocked |= gm;
@@ -536,14 +545,11 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
                     gd.mat_off = alloc(d * d);
                     out.events[g.special_event].mat_off = gd.mat_off;
                 } else {
-                    // tensor cores: pad the fused gate to 4 qubits with the lowest
-                    // qubits it does not touch (always inside the tile)
-                    uint64_t pm = g.mask;
-                    if (P.tc)
-                        for (int q = 0; q < n && popc(pm) < P.tc_k; ++q) pm |= 1ull << q;
+                    // tensor cores: pad the fused gate to tc_k qubits (inside the tile)
+                    const uint64_t pm = padded(g);
                     const int d = 1 << popc(pm);
-                    // tensor cores: W hi/lo operand, gate_bytes(tc_k) = 2 * (2^(k+1))^2 * 4 B
-                    gd.mat_off = alloc(P.tc ? (2 << P.tc_k) * (2 << P.tc_k) : d * d);
+                    // tensor cores: the GEMM operand, tc_gate_bytes(tc_k) bytes (complex64 units)
+                    gd.mat_off = alloc(P.tc ? tc_gate_bytes(P.tc_k) / 8 : d * d);
                     FusedDesc fd;
                     fd.mat_off = gd.mat_off;
                     fd.k = popc(pm) | (P.tc ? kGateTC : 0);
@@ -602,7 +608,9 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
             pd.tile_mask = fill_tile(pd.tile_mask, T, n);
             for (int g = 0; g < pd.gate_count; ++g) {
                 GateDesc& gd = out.gates[pd.gate_begin + g];
-                gate_layout(gate_masks[pd.gate_begin + g], pd.tile_mask, T, P.R, gd.rpos, gd.tpos);
+                // 6-qubit tensor-core gates: every gate bit in registers (R = 6)
+                const int R = (P.tc && P.tc_k == 6 && (gd.k & kGateTC)) ? 6 : P.R;
+                gate_layout(gate_masks[pd.gate_begin + g], pd.tile_mask, T, R, gd.rpos, gd.tpos);
             }
             if (P.tc && P.tc_k == 4) {
                 tc_runs(out.gates.data() + pd.gate_begin, gate_norms.data() + pd.gate_begin, pd.gate_count, T);

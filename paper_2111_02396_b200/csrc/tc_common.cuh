@@ -15,14 +15,20 @@
 // both live in shared memory in the SWIZZLE_128B K-major layout (one 128-byte
 // row per subvector / output column, 8-row atoms of 1024 B).
 //
-// 5-qubit gates (kind::tf32, f = 5 plans): U (32 x 32 complex) applied to the
-// 128 subvectors x_s of a tile is the real GEMM  Y~ = X~ W  with
-//   X~[s][2c + re/im] = x_s[c]   (M = 128 rows, K = 64),
-//   W[2c + a][2j + b]  = the real 2x2 block of U[j][c] (N = 64),
-// one tcgen05.mma.kind::tf32 chain (A = X~ in TMEM, B = W in shared memory,
-// D in TMEM), K split into 8 K-steps of 8.  Single precision is kept by
-// 3xTF32: X~ = Xh + Xl, W = Wh + Wl (hi/lo tf32), D = Xh Wh + Xl Wh + Xh Wl
-// (the dropped Xl Wl term is ~2^-24 relative).
+// 5- and 6-qubit gates (kind::f16, f = 5 / 6 plans; "wide" gates, one gate at
+// a time): U (2^k x 2^k complex) applied to the subvectors x_s of a tile is the
+// real GEMM Y = X W^T with X[s][2c + a] = component a of x_s[c] and
+// W[2j + b][2c + a] = the real 2x2 block of U[j][c] (input component a, output
+// component b).  Single precision is kept with f16 hi / lo splits of the
+// (tile-scaled) amplitudes and of W:  Y = Xh Wh + Xl Wh + Xh Wl (+ Xl Wl).
+//   k = 5: 128 subvectors = M; K = N = 64.  A = [Xh | Xl] as two 16 KB
+//          K-chunks, B = [Wh | Wl] as two 8 KB parts; 3 x 4 MMAs M128 N64 K16
+//          accumulate into one 64-column D.
+//   k = 6: 64 subvectors, K = N = 128.  The MMA rows are (part, subvector):
+//          rows 0..63 = Xh, rows 64..127 = Xl; B rows 0..127 = Wh, 128..255 =
+//          Wl, so one N = 256 chain (8 K-steps, two 16 KB A chunks / two 32 KB
+//          B chunks) gives all four products; the epilogue adds row s and row
+//          s + 64 (an exchange through shared memory between threads t, t ^ 64).
 #pragma once
 #include <stdint.h>
 
@@ -52,14 +58,22 @@ __host__ __device__ __forceinline__ uint32_t w_offset_bytes(int n, int k) {
 constexpr int kWBytes = 32 * 32 * 4;          // one of hi / lo
 constexpr int kGateBytes = 2 * kWBytes;       // hi then lo (8 KB)
 
-// General k-qubit gate (k = 4, 5): N = K = 2^(k+1).  W is stored as K/32 chunks
-// of [N rows][32 tf32] (each chunk a SWIZZLE_128B K-major block), hi part then lo.
+// tf32 hi / lo W of a 4-qubit gate (3xTF32, single-gate runs): N = K = 32,
+// one [N rows][32 tf32] SWIZZLE_128B K-major block per part, hi then lo.
 __host__ __device__ __forceinline__ uint32_t w_offset_bytes_k(int k, int n, int kk) {
     const int N = 2 << k;
     return (uint32_t)((kk >> 5) * N * 128) + w_offset_bytes(n, kk & 31);
 }
 __host__ __device__ constexpr int w_part_bytes(int k) { return (2 << k) * (2 << k) * 4; }
-__host__ __device__ constexpr int gate_bytes(int k) { return 2 * w_part_bytes(k); }
+// Pool / shared-memory bytes of a tensor-core gate operand: k = 4: 8 KB (f16
+// B or tf32 hi/lo W); k = 5: 2 x [64][64] f16 = 16 KB; k = 6: 2 K-chunks of
+// [256][64] f16 = 64 KB.
+__host__ __device__ constexpr int gate_bytes(int k) { return k <= 4 ? 2 * w_part_bytes(4) : (k == 5 ? 16384 : 65536); }
+// Byte offset of f16 element (row n, K index kk) of a wide-gate B operand.
+__host__ __device__ __forceinline__ uint32_t wide_b_offset(int k, int part, int n, int kk) {
+    return k == 5 ? (uint32_t)(part * 8192) + sw128_offset(n, 2 * kk)
+                  : (uint32_t)((kk >> 6) * 32768) + sw128_offset(part * 128 + n, 2 * (kk & 63));
+}
 
 // Instruction descriptor: kind::tf32, D f32, A/B tf32 K-major, M = 128, N.
 __host__ __device__ constexpr uint32_t idesc_tf32_m128(int N) {

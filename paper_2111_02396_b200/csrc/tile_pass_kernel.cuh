@@ -388,52 +388,107 @@ __device__ __forceinline__ void apply_tc_gate(float2* tile, uint32_t w_smem, uin
     fence_before();
 }
 
-// Apply one padded 5-qubit gate on tensor cores (128 threads): thread t owns
-// subvector s = t of 32 amplitudes (register bits 0..4 = the gate bits), TMEM
-// lane t.  N = K = 64: TMEM columns D [0,64), A hi [64,128), A lo [128,192);
-// W in shared memory as two K-chunks of [64][32] tf32 (hi, then lo at +16 KB).
-__device__ __forceinline__ void apply_tc_gate5(float2* tile, uint32_t w_smem, uint32_t pbase,
-                                               const uint32_t (&unit)[5], uint32_t tmem, uint64_t* mbar,
-                                               uint32_t& phase) {
+// Apply one padded K-qubit gate (K = 5, 6) on tensor cores with f16 hi / lo
+// operands (tc_common.cuh "wide" gates), 128 threads.  Layout (host-computed,
+// R = K): register bits 0..K-1 = the gate bits, thread bits = the other 12 - K
+// tile bits.  K = 5: thread t owns subvector t (32 configurations) = MMA row t.
+// K = 6: thread t owns configurations 32 h .. 32 h + 31 (h = t >> 6, gate bit
+// 5) of subvector s = t & 63; MMA rows s / s + 64 hold its hi / lo parts.  The
+// tile is converted in place with a power-of-two tile scale (as a f16 run
+// start), the MMAs read A = the tile and B = W from shared memory, and the
+// epilogue writes the fp32 tile back.  K = 6 exchanges half of each row's
+// outputs through wbuf (free once the MMAs are done).
+template <int K>
+__device__ __forceinline__ void apply_tc_wide(float2* tile, unsigned char* wbuf, const GateDesc& G, uint32_t tmem,
+                                              uint64_t* mbar, uint32_t& phase, double* red) {
     using namespace tc;
-    const int tid = threadIdx.x;
+    static_assert(K == 5 || K == 6, "wide tensor-core gates are 5 or 6 qubits");
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
     char* const tb8 = reinterpret_cast<char*>(tile);
+    const uint32_t tile_s = (uint32_t)__cvta_generic_to_shared(tile);
+    const uint32_t w_s = (uint32_t)__cvta_generic_to_shared(wbuf);
+    uint32_t unit[K];
+#pragma unroll
+    for (int m = 0; m < K; ++m) unit[m] = swz(1u << ((G.rpos >> (4 * m)) & 15u)) << 3;
+    uint32_t tb = 0;
+#pragma unroll
+    for (int i = 0; i < 12 - K; ++i) tb |= ((tid >> i) & 1u) << ((G.tpos >> (4 * i)) & 15u);
+    const uint32_t h = K == 6 ? (tid >> 6) : 0u;
+    uint32_t base = swz(tb) << 3;
+    if constexpr (K == 6) base ^= h ? unit[K - 1] : 0u;
     uint32_t lo[32];
-    lo[0] = pbase;
+    lo[0] = 0;
 #pragma unroll
     for (int m = 0; m < 5; ++m)
 #pragma unroll
         for (int x = 0; x < (1 << m); ++x) lo[x + (1 << m)] = lo[x] ^ unit[m];
-    const uint32_t lane = (uint32_t)(tid & 96) << 16;
+    float run_inv;
+    {
+        float2 v[32];
+        float amax = 0.f;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {  // configurations 16 h .. 16 h + 15 = A columns 32 h .. 32 h + 31
-        uint32_t hi[32], lw[32];
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-            const float2 v = *reinterpret_cast<const float2*>(tb8 + lo[16 * h + c]);
-            const uint32_t hx = __float_as_uint(v.x) & 0xFFFFE000u, hy = __float_as_uint(v.y) & 0xFFFFE000u;
-            hi[2 * c] = hx;
-            hi[2 * c + 1] = hy;
-            lw[2 * c] = __float_as_uint(v.x - __uint_as_float(hx));
-            lw[2 * c + 1] = __float_as_uint(v.y - __uint_as_float(hy));
+        for (int c = 0; c < 32; ++c) {
+            v[c] = *reinterpret_cast<const float2*>(tb8 + (base ^ lo[c]));
+            amax = fmaxf(amax, fmaxf(fabsf(v[c].x), fabsf(v[c].y)));
         }
-        tmem_st32(tmem + lane + 64 + 32 * h, hi);
-        tmem_st32(tmem + lane + 128 + 32 * h, lw);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        float* redf = reinterpret_cast<float*>(red);
+        if (lane == 0) redf[warp] = amax;
+        __syncthreads();  // every fp32 read done (in-place rewrite below) + maxima visible
+        amax = fmaxf(fmaxf(redf[0], redf[1]), fmaxf(redf[2], redf[3]));
+        const int shift = (G.k >> kGateShiftBit) & 0xff;
+        int se = 260 - (int)((__float_as_uint(amax) >> 23) & 0xffu) - shift;  // amax * 2^(se - 127) in [2^6, 2^7)
+        se = min(max(se, 1), 253);
+        const float run_scale = __uint_as_float((uint32_t)se << 23);
+        run_inv = __uint_as_float((uint32_t)(254 - se) << 23);
+        const uint64_t sc2 = pk2(run_scale, run_scale);
+        // A rows: K = 5: row t, hi in chunk 0, lo in chunk 1 (16 KB); K = 6: rows
+        // s (hi) and s + 64 (lo) of chunk h.  Four configurations per 16-byte store.
+        const uint32_t row = K == 5 ? tid : (tid & 63u);
+        const uint32_t hi_base = K == 5 ? 0u : h * (uint32_t)kF16GroupBytes;
+        const uint32_t lo_base = K == 5 ? (uint32_t)kF16GroupBytes : h * (uint32_t)kF16GroupBytes;
+        const uint32_t lo_row = K == 5 ? row : row + 64u;
+#pragma unroll
+        for (int c4 = 0; c4 < 8; ++c4) {
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint2 sp = split_f16(mul2(pk2(v[4 * c4 + j].x, v[4 * c4 + j].y), sc2));
+                hw[j] = sp.x;
+                lw[j] = sp.y;
+            }
+            *reinterpret_cast<uint4*>(tb8 + hi_base + sw128_offset((int)row, 16 * c4)) =
+                make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(tb8 + lo_base + sw128_offset((int)lo_row, 16 * c4)) =
+                make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        }
+        fence_proxy_async();
+        fence_before();
+        __syncthreads();
     }
-    tmem_wait_st();
-    fence_before();
-    __syncthreads();
     if (tid == 0) {
         fence_after();
-        constexpr uint32_t idesc = idesc_tf32_m128(64);
+        if constexpr (K == 5) {
+            constexpr uint32_t idesc = idesc_f16_m128(64);
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-            const uint32_t off = (uint32_t)((ks >> 2) * 8192 + (ks & 3) * 32);
-            const uint64_t bh = smem_desc_sw128(w_smem + off);
-            const uint64_t bl = smem_desc_sw128(w_smem + (uint32_t)w_part_bytes(5) + off);
-            mma_tf32_ts_n(tmem, tmem + 64 + ks * 8, bh, idesc, ks > 0);
-            mma_tf32_ts_n(tmem, tmem + 128 + ks * 8, bh, idesc, 1);
-            mma_tf32_ts_n(tmem, tmem + 64 + ks * 8, bl, idesc, 1);
+            for (int ks = 0; ks < 4; ++ks) {
+                const uint64_t ah = smem_desc_sw128(tile_s + ks * 32);
+                const uint64_t al = smem_desc_sw128(tile_s + kF16GroupBytes + ks * 32);
+                const uint64_t bh = smem_desc_sw128(w_s + ks * 32);
+                const uint64_t bl = smem_desc_sw128(w_s + 8192 + ks * 32);
+                mma_f16_ss(tmem, ah, bh, idesc, ks > 0);
+                mma_f16_ss(tmem, al, bh, idesc, 1);
+                mma_f16_ss(tmem, ah, bl, idesc, 1);
+            }
+        } else {
+            constexpr uint32_t idesc = idesc_f16_m128(256);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const uint32_t off = (uint32_t)((ks & 3) * 32);
+                mma_f16_ss(tmem, smem_desc_sw128(tile_s + (ks >> 2) * kF16GroupBytes + off),
+                           smem_desc_sw128(w_s + (ks >> 2) * 32768 + off), idesc, ks > 0);
+            }
         }
         mma_commit(mbar);
     }
@@ -441,15 +496,51 @@ __device__ __forceinline__ void apply_tc_gate5(float2* tile, uint32_t w_smem, ui
     mbar_wait(mbar, phase);
     phase ^= 1u;
     fence_after();
+    const uint32_t lane_off = (warp * 32u) << 16;
+    const uint64_t inv2 = pk2(run_inv, run_inv);
+    if constexpr (K == 5) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        uint32_t v[32];
-        tmem_ld32(tmem + lane + 32 * h, v);
-        tmem_wait_ld();
+        for (int p = 0; p < 2; ++p) {
+            uint32_t d[32];
+            tmem_ld32(tmem + lane_off + 32 * p, d);
+            tmem_wait_ld();
 #pragma unroll
-        for (int c = 0; c < 16; ++c)
-            *reinterpret_cast<float2*>(tb8 + lo[16 * h + c]) =
-                make_float2(__uint_as_float(v[2 * c]), __uint_as_float(v[2 * c + 1]));
+            for (int c = 0; c < 16; ++c)
+                *reinterpret_cast<float2*>(tb8 + (base ^ lo[16 * p + c])) =
+                    upk2(mul2(pk2(__uint_as_float(d[2 * c]), __uint_as_float(d[2 * c + 1])), inv2));
+        }
+    } else {
+        // row t holds (hi or lo part) x W_hi in columns [0, 128) and x W_lo in
+        // [128, 256); output column n = 2 j + b.  Thread t keeps the outputs of its
+        // configuration half (columns 64 h ..) and sends the other half to t ^ 64.
+        float* xbuf = reinterpret_cast<float*>(wbuf);
+        const uint32_t sh = 64u * (h ^ 1u), kh = 64u * h;
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            uint32_t a[32], b[32];
+            tmem_ld32(tmem + lane_off + sh + 32 * p, a);
+            tmem_ld32(tmem + lane_off + 128 + sh + 32 * p, b);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                xbuf[(32 * p + i) * 128 + (tid ^ 64u)] = __uint_as_float(a[i]) + __uint_as_float(b[i]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            uint32_t a[32], b[32];
+            tmem_ld32(tmem + lane_off + kh + 32 * p, a);
+            tmem_ld32(tmem + lane_off + 128 + kh + 32 * p, b);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                const float yr = (__uint_as_float(a[2 * c]) + __uint_as_float(b[2 * c])) +
+                                 xbuf[(32 * p + 2 * c) * 128 + tid];
+                const float yi = (__uint_as_float(a[2 * c + 1]) + __uint_as_float(b[2 * c + 1])) +
+                                 xbuf[(32 * p + 2 * c + 1) * 128 + tid];
+                *reinterpret_cast<float2*>(tb8 + (base ^ lo[16 * p + c])) = upk2(mul2(pk2(yr, yi), inv2));
+            }
+        }
     }
     fence_before();
 }
@@ -463,25 +554,28 @@ struct TileCfg {
     static constexpr int TILE = 1 << T;
     static constexpr int CL = T < detail::kCL ? T : detail::kCL;
     static constexpr int NH = TILE >> CL;
-    // shared memory: [W/matrix buffers x2][tile][hoff][red][gdesc][mbar], base 1024-aligned
+    // shared memory: [W/matrix buffers x2 (x1 for 6-qubit tensor-core gates: 64 KB)]
+    // [tile][hoff][red][gdesc][mbar], base 1024-aligned
     static constexpr size_t kMbufBytes = TC ? (size_t)tc::gate_bytes(TCK) : sizeof(float2) * ((size_t)1 << (2 * R));
-    static constexpr size_t kTileOff = 2 * kMbufBytes;
+    static constexpr int kNumMbuf = (TC && TCK == 6) ? 1 : 2;
+    static constexpr size_t kTileOff = kNumMbuf * kMbufBytes;
     static constexpr size_t kHoffOff = kTileOff + sizeof(float2) * TILE;
     static constexpr size_t kRedOff = kHoffOff + sizeof(uint64_t) * ((NH + 1) & ~1);
     static constexpr size_t kGdescOff = kRedOff + 64 * sizeof(double);
     static constexpr size_t kMbarOff = kGdescOff + sizeof(GateDesc) * kMaxPassGates;
     static_assert(!TC || TCK != 4 || tc::gate_bytes(4) == tc::kF16GateBytes, "f16 operand size");
+    static_assert(!TC || tc::gate_bytes(TCK) == tc_gate_bytes(TCK), "operand size (desc.hpp)");
     static constexpr size_t kBytes = kMbarOff + 16 + 1024;  // 2 mbarriers + alignment slack
 };
 
 template <int T, int R, bool TC, int TCK = 4>
 __global__ void __launch_bounds__(TileCfg<T, R, TC, TCK>::NT,
-                                  TC ? (TCK == 5 ? 2 : 4) : ((R <= 4 && T == 12) ? QT_MINB : 1))
+                                  TC ? (TCK == 6 ? 2 : (TCK == 5 ? 3 : 4)) : ((R <= 4 && T == 12) ? QT_MINB : 1))
 tile_pass_kernel(const TileArgs A, const int step) {
     using Cfg = TileCfg<T, R, TC, TCK>;
     // TMEM: TCK = 4: f16 runs use D of both groups (2 x 64 columns), 3xTF32 single
-    // gates D0 / D1 / A hi / A lo (4 x 32); TCK = 5: D 64 + A hi/lo 128
-    constexpr uint32_t kTmemCols = TCK == 5 ? 256 : 128;  // CTAs per SM share 512 columns
+    // gates D0 / D1 / A hi / A lo (4 x 32); TCK = 5: D (64); TCK = 6: D (256)
+    constexpr uint32_t kTmemCols = TCK == 6 ? 256 : (TCK == 5 ? 64 : 128);  // CTAs per SM share 512 columns
     constexpr int NT = Cfg::NT;
     constexpr int NA = Cfg::NA;
     constexpr int CL = Cfg::CL;
@@ -509,7 +603,7 @@ tile_pass_kernel(const TileArgs A, const int step) {
     // shared address space: LDS/STS instead of generic LD/ST)
     const uint32_t smem_base = (uint32_t)__cvta_generic_to_shared(smem_raw);
     unsigned char* sm = smem_raw + (((smem_base + 1023u) & ~1023u) - smem_base);
-    unsigned char* mbuf = sm;  // 2 x kMbufBytes
+    unsigned char* mbuf = sm;  // kNumMbuf x kMbufBytes
     float2* tile = reinterpret_cast<float2*>(sm + Cfg::kTileOff);
     uint64_t* hoff = reinterpret_cast<uint64_t*>(sm + Cfg::kHoffOff);
     double* red = reinterpret_cast<double*>(sm + Cfg::kRedOff);
@@ -583,29 +677,44 @@ tile_pass_kernel(const TileArgs A, const int step) {
         }
     }
     cp_async_commit();
-    cp_async_wait_all();  // gate descriptors + tile
-    __syncthreads();
-    QT_KMARK(2);
     auto mat_bytes = [](const GateDesc& G) -> int {
         return (TC && (G.k & kGateTC)) ? tc::gate_bytes(TCK) : (int)sizeof(float2) * (1 << (2 * (G.k & 0xff)));
     };
+    if (ng > 0) {  // the first gate's matrix travels with the tile (descriptor read from global)
+        const GateDesc& G0 = A.gates[P.gate_begin];
+        const char* src = reinterpret_cast<const char*>(A.pool + G0.mat_off);
+        const int chunks = mat_bytes(G0) >> 4;
+        for (int c = tid; c < chunks; c += NT) cp_async16(mbuf + 16 * c, src + 16 * c);
+        cp_async_commit();
+    }
+    cp_async_wait_all();  // gate descriptors + tile + W(0)
+    __syncthreads();
+    QT_KMARK(2);
     // gate matrices: double-buffered, cooperative cp.async (measured faster than
     // one-thread bulk copies completing on an mbarrier)
     auto load_w = [&](int g) {
-        unsigned char* dst = mbuf + (g & 1) * Cfg::kMbufBytes;
+        unsigned char* dst = mbuf + (Cfg::kNumMbuf == 2 ? (g & 1) * Cfg::kMbufBytes : 0);
         const char* src = reinterpret_cast<const char*>(A.pool + gdesc[g].mat_off);
         const int chunks = mat_bytes(gdesc[g]) >> 4;
         for (int c = tid; c < chunks; c += NT) cp_async16(dst + 16 * c, src + 16 * c);
         cp_async_commit();
     };
-    if (ng > 0) load_w(0);
     for (int gi = 0; gi < ng; ++gi) {
         const GateDesc& G = gdesc[gi];
         cp_async_wait_all();
         if constexpr (TC) tc::fence_proxy_async();  // cp.async W / st.shared rows -> tensor-core reads
         __syncthreads();  // tile writes of the previous gate visible; W buffer (gi + 1) & 1 free
-        if (gi + 1 < ng) load_w(gi + 1);
-        unsigned char* mcur = mbuf + (gi & 1) * Cfg::kMbufBytes;
+        if constexpr (Cfg::kNumMbuf == 1) {  // one W buffer: gate gi's matrix is loaded now
+            if (gi > 0) {
+                load_w(gi);
+                cp_async_wait_all();
+                tc::fence_proxy_async();
+                __syncthreads();
+            }
+        } else if (gi + 1 < ng) {
+            load_w(gi + 1);
+        }
+        unsigned char* mcur = mbuf + (Cfg::kNumMbuf == 2 ? (gi & 1) * Cfg::kMbufBytes : 0);
         if constexpr (TC && TCK == 4) {
             if (G.k & kGateF16) {  // run start (runs end before any non-f16 gate)
                 gi = tc_run_f16<T>(tile, mbuf, (uint32_t)Cfg::kMbufBytes, gdesc, gi, ng, A.pool, tmem, mbar, ph, red,
@@ -626,9 +735,8 @@ tile_pass_kernel(const TileArgs A, const int step) {
                 if constexpr (R == 5 && TCK == 4)
                     apply_tc_gate(tile, (uint32_t)__cvta_generic_to_shared(mcur), swz(tb) << 3, unit, tmem, mbar,
                                   ph[0]);
-                else if constexpr (R == 5 && TCK == 5)
-                    apply_tc_gate5(tile, (uint32_t)__cvta_generic_to_shared(mcur), swz(tb) << 3, unit, tmem, mbar,
-                                   ph[0]);
+                else if constexpr (R == 5 && (TCK == 5 || TCK == 6))
+                    apply_tc_wide<TCK>(tile, mcur, G, tmem, mbar, ph[0], red);
             } else if ((G.k & 0xff) == 1) {  // device-chosen conventional operators (q <= 2)
                 apply_fused<1, R>(tile, reinterpret_cast<const float2*>(mcur), swz(tb) << 3, unit);
             } else {
@@ -823,7 +931,7 @@ inline size_t tile_pass_smem_bytes_impl(int T, int R, bool tcm, int tck = 4) {
     const int CL = T < detail::kCL ? T : detail::kCL;
     const size_t mb = tcm ? (size_t)tc::gate_bytes(tck) : sizeof(float2) * ((size_t)1 << (2 * R));
     const size_t nh = ((((size_t)1 << T) >> CL) + 1) & ~(size_t)1;
-    return 2 * mb + (sizeof(float2) << T) + sizeof(uint64_t) * nh + 64 * sizeof(double) +
+    return (tcm && tck == 6 ? 1 : 2) * mb + (sizeof(float2) << T) + sizeof(uint64_t) * nh + 64 * sizeof(double) +
            sizeof(GateDesc) * kMaxPassGates + 16 + 1024;
 }
 

@@ -234,24 +234,24 @@ def test_config2_sample_of_trajectories(ctx):
 # tiny amplitudes and all-zero tiles; chains of 4-qubit operators applied with
 # qt_apply_plan vs the oracle's Alg. 1 one operator at a time.
 # ---------------------------------------------------------------------------
-def _chain(rng, n_ops, low=12):
+def _chain(rng, n_ops, low=12, k=4):
     ops = []
     prev = None
     for _ in range(n_ops):
         while True:
-            qs = sorted(int(x) for x in rng.choice(low, 4, replace=False))
+            qs = sorted(int(x) for x in rng.choice(low, k, replace=False))
             if qs != prev:
                 break
         prev = qs
-        ops.append((qs, workloads.haar_unitary(rng, 16)))
+        ops.append((qs, workloads.haar_unitary(rng, 2 ** k)))
     return ops
 
 
-def _apply_chain(ctx, psi, ops, n):
+def _apply_chain(ctx, psi, ops, n, f=4):
     c = qtraj.Circuit(n)
     for m, (qs, M) in enumerate(ops):
         c.add_matrix(m, qs, M)
-    plan = qtraj.Plan(c, max_fused=4)
+    plan = qtraj.Plan(c, max_fused=f, tensor_cores=1)
     d = to_dev(psi)
     ctx.apply_plan(plan, d)
     ref = psi.copy()
@@ -282,6 +282,41 @@ def test_tc_run_amplitude_range(ctx, amp):
     rng = np.random.default_rng(11)
     got, ref = _apply_chain(ctx, rand_state(rng, n) * amp, _chain(rng, 10), n)
     assert rel_l2(got, ref) < AMP_TOL, rel_l2(got, ref)
+
+
+@pytest.mark.parametrize("k", [5, 6])
+@pytest.mark.parametrize("amp", [1e-25, 1.0, 1e3])
+def test_tc_wide_gates_amplitude_range(ctx, k, amp):
+    """5- and 6-qubit tensor-core gates (f16 hi/lo GEMMs, tile scale per gate):
+    chains of Haar k-qubit operators on high and low qubits, any amplitude scale."""
+    n = 15
+    rng = np.random.default_rng(20 + k)
+    ops = _chain(rng, 5, low=n, k=k)
+    got, ref = _apply_chain(ctx, rand_state(rng, n) * amp, ops, n, f=k)
+    assert rel_l2(got, ref) < AMP_TOL, rel_l2(got, ref)
+
+
+@pytest.mark.parametrize("k", [5, 6])
+def test_tc_wide_gates_norm_growth(ctx, k):
+    """Non-unitary k-qubit operators (norm up to 40) on the wide tensor-core path."""
+    n = 14
+    rng = np.random.default_rng(30 + k)
+    ops = [(qs, M * (40.0 if i % 2 == 0 else 1.0)) for i, (qs, M) in enumerate(_chain(rng, 4, low=n, k=k))]
+    got, ref = _apply_chain(ctx, rand_state(rng, n), ops, n, f=k)
+    assert np.all(np.isfinite(got))
+    assert rel_l2(got, ref) < AMP_TOL, rel_l2(got, ref)
+
+
+@pytest.mark.parametrize("f", [5, 6])
+@pytest.mark.parametrize("tensor_cores", [-1, 1])
+def test_wide_fused_gates_trajectories(ctx, f, tensor_cores):
+    """Noisy trajectories with fused gates of up to f = 5 / 6 qubits (3-qubit
+    operators included) on tcgen05 (f16 hi/lo, padded to f qubits) and on CUDA
+    cores: identical Kraus choices and samples, states within 1e-5."""
+    c = workloads.random_circuit(14, depth=8, seed=500 + f, max_arity=3, noise="both", p=0.03,
+                                 t1_ns=800.0, tphi_ns=1400.0, readout=True)
+    ref, out, state = run_both(ctx, c, seed=19, T=8, shots=2, f=f, tensor_cores=tensor_cores)
+    compare(ref, out, state)
 
 
 def test_tc_run_zero_tiles(ctx):
