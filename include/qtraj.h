@@ -111,6 +111,19 @@ qt_status qt_add_channel(qt_circuit c, int moment, int nq, const int* qubits, in
 /* Readout errors: p00_err[q] = probability |0> is recorded as 1,
  * p11_err[q] = probability |1> is recorded as 0.  Either may be NULL. */
 qt_status qt_set_readout(qt_circuit c, const double* p00_err, const double* p11_err);
+/* Parametrized circuits "for many different choices of parameters": a
+ * sweep gate carries n_sets unitaries U[s] (n_sets consecutive 2^nq x 2^nq
+ * complex128 matrices, layout as qt_add_gate; copied at call time).  Trajectory
+ * t of qt_run_trajectories applies U[t mod n_sets], so one call runs every
+ * parameter set (interleaved) and each record is a pure function of (circuit,
+ * seed, t) as for plain circuits; sweep gates draw no random numbers, so set s
+ * of the sweep reproduces trajectories t = s (mod n_sets) of the circuit with
+ * U[s] in place of the sweep gate.  All sweep gates of a circuit have the same
+ * n_sets (else QT_EINVAL); n_sets = 1 is qt_add_gate.  QT_ENONUNITARY if any
+ * U[s] is not unitary (1e-9).  qt_circuit_num_sets returns n_sets (1 without
+ * sweep gates). */
+qt_status qt_add_gate_sweep(qt_circuit c, int moment, int nq, const int* qubits, int n_sets, const double* U);
+int qt_circuit_num_sets(qt_circuit c);
 /* Number of channels whose record flag is set (columns of out_kraus). */
 int qt_circuit_num_recorded(qt_circuit c);
 int qt_circuit_num_channels(qt_circuit c);

@@ -198,6 +198,38 @@ qt_status qt_add_gate(qt_circuit c, int moment, int nq, const int* qubits, const
     return QT_OK;
 }
 
+qt_status qt_add_gate_sweep(qt_circuit c, int moment, int nq, const int* qubits, int n_sets, const double* U) {
+    if (!c || !U) return fail(QT_EINVAL, "NULL argument");
+    if (n_sets < 1 || n_sets > (1 << 20)) return fail(QT_EINVAL, "n_sets must be 1..2^20");
+    if (c->c.n_sets > 1 && n_sets > 1 && n_sets != c->c.n_sets)
+        return fail(QT_EINVAL, "every sweep gate of a circuit must have the same number of parameter sets");
+    uint64_t mask;
+    qt_status st = check_qubits(c, moment, nq, qubits, &mask);
+    if (st != QT_OK) return st;
+    HostOp op;
+    op.kind = 0;
+    op.moment = moment;
+    op.seq = c->c.seq++;
+    op.nq = nq;
+    op.mask = mask;
+    op.n_kraus = n_sets;
+    const int d = 1 << nq;
+    op.mats.resize((size_t)n_sets * d * d);
+    for (int set = 0; set < n_sets; ++set) {
+        cd* m = op.mats.data() + (size_t)set * d * d;
+        canonicalize(nq, qubits, U + (size_t)set * 2 * d * d, op.q, m);
+        const cd* cm = m;
+        if (!(max_dev_from_identity_of_gram(d, &cm, 1) < 1e-9))
+            return fail(QT_ENONUNITARY, "sweep gate matrix " + std::to_string(set) + " is not unitary (tolerance 1e-9)");
+    }
+    c->moment_mask[moment] |= mask;
+    if (n_sets > 1) c->c.n_sets = n_sets;
+    c->c.ops.push_back(std::move(op));
+    return QT_OK;
+}
+
+int qt_circuit_num_sets(qt_circuit c) { return c ? c->c.n_sets : 0; }
+
 double qt_draw(uint64_t seed, uint32_t ordinal, uint32_t purpose, uint64_t traj, int half) {
     return draw(seed, ordinal, purpose, traj, half);
 }
@@ -516,28 +548,31 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
             }
             P.chans.push_back(cdsc);
         } else {
-            Variant v;
-            v.nq = hop->nq;
-            VarDesc vd;
-            vd.off = (int)(P.var_data.size() / 2);
-            vd.nq = hop->nq;
-            bool ident = true;
-            for (int e = 0; e < d * d; ++e) {
-                P.var_data.push_back(hop->mats[e].real());
-                P.var_data.push_back(hop->mats[e].imag());
-                const cd target = (e / d == e % d) ? cd(1, 0) : cd(0, 0);
-                if (std::abs(hop->mats[e] - target) > 1e-15) ident = false;
+            // one variant per parameter set (plain gates: one)
+            for (int set = 0; set < hop->n_kraus; ++set) {
+                const cd* M = hop->mats.data() + (size_t)set * d * d;
+                Variant v;
+                v.nq = hop->nq;
+                VarDesc vd;
+                vd.off = (int)(P.var_data.size() / 2);
+                vd.nq = hop->nq;
+                bool ident = true;
+                for (int e = 0; e < d * d; ++e) {
+                    P.var_data.push_back(M[e].real());
+                    P.var_data.push_back(M[e].imag());
+                    const cd target = (e / d == e % d) ? cd(1, 0) : cd(0, 0);
+                    if (std::abs(M[e] - target) > 1e-15) ident = false;
+                }
+                v.identity = ident;
+                // qt_add_matrix operations may have any norm: Frobenius bound unless unitary
+                if (!(max_dev_from_identity_of_gram(d, &M, 1) < 1e-9)) {
+                    double fro = 0;
+                    for (int e = 0; e < d * d; ++e) fro += std::norm(M[e]);
+                    v.norm = std::max(1.0, std::sqrt(fro));
+                }
+                P.vars.push_back(v);
+                P.var_desc.push_back(vd);
             }
-            v.identity = ident;
-            // qt_add_matrix operations may have any norm: Frobenius bound unless unitary
-            const cd* m = hop->mats.data();
-            if (!(max_dev_from_identity_of_gram(d, &m, 1) < 1e-9)) {
-                double fro = 0;
-                for (int e = 0; e < d * d; ++e) fro += std::norm(hop->mats[e]);
-                v.norm = std::max(1.0, std::sqrt(fro));
-            }
-            P.vars.push_back(v);
-            P.var_desc.push_back(vd);
         }
         P.ops.push_back(std::move(po));
     }
@@ -556,6 +591,7 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
                 break;
             }
     P.n_channels = chan;
+    P.n_sets = C.n_sets;
     P.n_recorded = rec;
     P.has_p00 = !C.p00.empty();
     P.has_p11 = !C.p11.empty();

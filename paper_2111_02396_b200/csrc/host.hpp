@@ -25,7 +25,7 @@ struct HostOp {
     int nq = 0;
     int q[6] = {0, 0, 0, 0, 0, 0};
     uint64_t mask = 0;
-    int n_kraus = 1;
+    int n_kraus = 1;       // channel: Kraus operators; gate: parameter sets (1 = plain gate)
     int record = 0;
     std::vector<cd> mats;  // n_kraus * d * d (internal order)
 };
@@ -35,6 +35,7 @@ struct Circuit {
     std::vector<HostOp> ops;
     std::vector<double> p00, p11;
     int seq = 0;
+    int n_sets = 1;  // parameter sets of sweep gates; trajectory t uses set t mod n_sets
 };
 
 // Plan-level operation (canonical order) with channel preprocessing.
@@ -77,6 +78,7 @@ struct Plan {
     int n_recorded = 0;
     int max_conv_d = 1;             // largest d of a non-mixture channel
     int max_chan_d = 1;             // largest d of any channel (conventional mode)
+    int n_sets = 1;                 // parameter sets (sweep gates pick variant traj mod n_sets)
     std::vector<double> p00, p11;
     bool has_p00 = false, has_p11 = false;
 };

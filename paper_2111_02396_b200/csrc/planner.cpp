@@ -423,8 +423,9 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
     std::vector<Barrier> barriers;
     for (const PlanOp& op : P.ops) {
         if (op.kind == 0) {
-            if (!P.vars[op.var_base].identity)
-                segs.back().push_back(Item{op.mask, op.var_base, -1, op.nq});
+            // sweep gates (P:262 parametrized circuits): variant = parameter set traj mod n_sets
+            const int v = op.var_base + (op.n_kraus > 1 ? (int)(traj % (uint64_t)P.n_sets) : 0);
+            if (!P.vars[v].identity) segs.back().push_back(Item{op.mask, v, -1, op.nq});
             continue;
         }
         const double u = draw(seed, (uint32_t)op.chan, kPurposeChannel, traj, 0);

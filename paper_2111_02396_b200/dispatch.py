@@ -52,6 +52,15 @@ def aggregate(obs: np.ndarray):
     return mean, se
 
 
+def aggregate_sets(obs: np.ndarray, n_sets: int, traj_begin: int = 0):
+    """Parameter sweeps: rows are trajectories traj_begin, traj_begin + 1, ...
+    (merged, trajectory order); trajectory t ran parameter set t mod n_sets.
+    Returns (mean, stderr), each [n_sets, n_obs]."""
+    t = traj_begin + np.arange(obs.shape[0])
+    out = [aggregate(obs[t % n_sets == s]) for s in range(n_sets)]
+    return np.stack([m for m, _ in out]), np.stack([e for _, e in out])
+
+
 def _gather_rows(t, group, world):
     """all_gather of a [count_r, ...] tensor whose counts differ by at most 1 across ranks."""
     import torch

@@ -81,6 +81,8 @@ def lib() -> ctypes.CDLL:
         "qt_add_channel": ([vp, ctypes.c_int, ctypes.c_int, ip, ctypes.c_int, dp, ctypes.c_int], ctypes.c_int),
         "qt_set_readout": ([vp, dp, dp], ctypes.c_int),
         "qt_circuit_num_recorded": ([vp], ctypes.c_int),
+        "qt_add_gate_sweep": ([vp, ctypes.c_int, ctypes.c_int, ip, ctypes.c_int, dp], ctypes.c_int),
+        "qt_circuit_num_sets": ([vp], ctypes.c_int),
         "qt_circuit_num_channels": ([vp], ctypes.c_int),
         "qt_fuse": ([vp, ctypes.c_int, ctypes.POINTER(vp)], ctypes.c_int),
         "qt_fuse_ex": ([vp, ctypes.POINTER(FuseOpts), ctypes.POINTER(vp)], ctypes.c_int),
@@ -150,6 +152,14 @@ class Circuit:
         m = _cplx(U)
         _check(lib().qt_add_gate(self.h, moment, len(q), _iptr(q), _dptr(m)))
 
+    def add_gate_sweep(self, moment: int, qubits: Sequence[int], Us: Iterable) -> None:
+        """Parametrized gate: one unitary per parameter set; trajectory t
+        applies Us[t mod n_sets]."""
+        q = np.asarray(qubits, np.int32)
+        ms = list(Us)
+        m = np.concatenate([_cplx(u) for u in ms])
+        _check(lib().qt_add_gate_sweep(self.h, moment, len(q), _iptr(q), len(ms), _dptr(m)))
+
     def add_matrix(self, moment: int, qubits: Sequence[int], M) -> None:
         """A general (e.g. non-unitary Kraus) operator; no unitarity check."""
         q = np.asarray(qubits, np.int32)
@@ -184,6 +194,10 @@ class Circuit:
     def num_channels(self) -> int:
         return lib().qt_circuit_num_channels(self.h)
 
+    @property
+    def num_sets(self) -> int:
+        return lib().qt_circuit_num_sets(self.h)
+
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:
             _lib.qt_circuit_destroy(self.h)
@@ -198,6 +212,8 @@ class Circuit:
             for op in moment:
                 if hasattr(op, "kraus"):
                     c.add_channel(mi, op.qubits, op.kraus, getattr(op, "record", True))
+                elif hasattr(op, "matrices"):
+                    c.add_gate_sweep(mi, op.qubits, op.matrices)
                 else:
                     c.add_gate(mi, op.qubits, op.matrix)
         if getattr(desc, "p00", None) is not None or getattr(desc, "p11", None) is not None:

@@ -30,6 +30,7 @@ __all__ = [
     "Gate", "Channel", "Circuit", "flatten", "gates", "channels",
     "ghz4_depolarized", "sycamore_grid_qcs", "low_noise_grid", "random_circuit",
     "circuit_seed", "trajectory_seed", "haar_unitary", "measurement", "circuit_to_json", "circuit_from_json",
+    "SweepGate", "n_sets", "resolve_set", "qaoa_grid_sweep",
 ]
 
 
@@ -46,6 +47,16 @@ class Gate:
     qubits: tuple
     matrix: np.ndarray  # (2^q, 2^q) complex128, Kronecker order of qubits
     name: str = "U"
+
+
+@dataclass
+class SweepGate:
+    """Parametrized gate ("parametrized circuits for many different choices of
+    parameters"): matrices[s] is the unitary of parameter set s; trajectory t of a
+    run uses set t mod len(matrices)."""
+    qubits: tuple
+    matrices: List[np.ndarray]  # each (2^q, 2^q) complex128, Kronecker order
+    name: str = "U(theta)"
 
 
 @dataclass
@@ -120,6 +131,22 @@ def flatten(c: Circuit):
     )
 
 
+def n_sets(c: Circuit) -> int:
+    """Parameter sets of a circuit's sweep gates (1 without sweep gates)."""
+    ns = {len(op.matrices) for op in c.ops() if isinstance(op, SweepGate)}
+    if len(ns) > 1:
+        raise ValueError("sweep gates with different numbers of parameter sets")
+    return ns.pop() if ns else 1
+
+
+def resolve_set(c: Circuit, s: int) -> Circuit:
+    """The plain circuit of parameter set s (each SweepGate -> Gate(matrices[s]));
+    no arithmetic, the matrices are copied as given."""
+    moms = [[Gate(op.qubits, op.matrices[s], op.name) if isinstance(op, SweepGate) else op for op in m]
+            for m in c.moments]
+    return Circuit(n_qubits=c.n_qubits, moments=moms, p00=c.p00, p11=c.p11, observables=list(c.observables))
+
+
 def measurement(qubit: int) -> Channel:
     """Mid-circuit computational-basis measurement of one qubit as a keyed channel
     (projectors; the record is the outcome, the state collapses, A12)."""
@@ -137,8 +164,8 @@ def _mat_from_json(d):
 
 
 def circuit_to_json(c: Circuit) -> str:
-    """Circuit file format (JSON): moments of gates ({"gate": name, "qubits", "matrix"})
-    and channels ({"channel": name, "qubits", "kraus": [...], "record"}), matrices in
+    """Circuit file format (JSON): moments of gates ({"gate": name, "qubits", "matrix"}),
+    sweep gates ({"sweep": name, "qubits", "matrices": [...]}) and channels ({"channel": name, "qubits", "kraus": [...], "record"}), matrices in
     Kronecker order of the listed qubits as {"re": rows, "im": rows}; optional
     readout p00 / p11 and observables (Pauli strings, char q = qubit q)."""
     import json
@@ -148,6 +175,9 @@ def circuit_to_json(c: Circuit) -> str:
         for op in m:
             if isinstance(op, Gate):
                 ops.append({"gate": op.name, "qubits": [int(q) for q in op.qubits], "matrix": _mat_to_json(op.matrix)})
+            elif isinstance(op, SweepGate):
+                ops.append({"sweep": op.name, "qubits": [int(q) for q in op.qubits],
+                            "matrices": [_mat_to_json(u) for u in op.matrices]})
             else:
                 ops.append({"channel": op.name, "qubits": [int(q) for q in op.qubits],
                             "kraus": [_mat_to_json(k) for k in op.kraus], "record": bool(op.record)})
@@ -172,6 +202,8 @@ def circuit_from_json(text: str) -> Circuit:
         for op in m:
             if "gate" in op:
                 ops.append(Gate(tuple(op["qubits"]), _mat_from_json(op["matrix"]), name=op["gate"]))
+            elif "sweep" in op:
+                ops.append(SweepGate(tuple(op["qubits"]), [_mat_from_json(u) for u in op["matrices"]], name=op["sweep"]))
             else:
                 ops.append(Channel(tuple(op["qubits"]), [_mat_from_json(k) for k in op["kraus"]],
                                    name=op["channel"], record=bool(op.get("record", True))))
@@ -355,4 +387,55 @@ def random_circuit(n: int, depth: int, seed: int, max_arity: int = 2,
         c.p00 = rng.uniform(0.005, 0.015, n)
         c.p11 = rng.uniform(0.03, 0.06, n)
     c.observables = ["I" * q + "Z" + "I" * (n - q - 1) for q in range(n)]
+    return c
+
+
+# ---------------------------------------------------------------------------
+# NEXT-4: parameter sweeps.  QAOA-style grid circuit (the paper's
+# "Hardware Grid" QAOA, as a circuit family only): |+>^n, then p
+# layers of exp(-i gamma Z Z) on every grid coupler (patterns A, B, C, D as
+# disjoint moments) and exp(-i beta X) mixers; (gamma_s, beta_s) per set s.
+# ---------------------------------------------------------------------------
+def zz_phase(gamma: float) -> np.ndarray:
+    """exp(-i gamma Z(x)Z) (diagonal)."""
+    return np.diag(np.exp(-1j * gamma * np.array([1.0, -1.0, -1.0, 1.0]))).astype(np.complex128)
+
+
+def x_mixer(beta: float) -> np.ndarray:
+    """exp(-i beta X)."""
+    c, s = np.cos(beta), np.sin(beta)
+    return np.array([[c, -1j * s], [-1j * s, c]], dtype=np.complex128)
+
+
+def qaoa_grid_sweep(rows: int, cols: int, layers: int, gammas: Sequence[Sequence[float]],
+                    betas: Sequence[Sequence[float]], depol: float = 1e-3, amp_damp: float = 0.0) -> Circuit:
+    """gammas[s][l], betas[s][l]: angles of layer l in parameter set s.  Noise:
+    depolarize(depol) after every 1q gate and on both qubits after every ZZ phase
+    (unitary mixtures), optional amplitude damping on every qubit per layer.
+    Observables: Z_a Z_b on every coupler."""
+    n = rows * cols
+    S = len(gammas)
+    assert len(betas) == S and all(len(g) == layers and len(b) == layers for g, b in zip(gammas, betas))
+    pat = _grid_couplers(rows, cols)
+    c = Circuit(n)
+    c.moments.append([Gate((q,), gates.H(), "H") for q in range(n)])
+    if depol > 0:
+        c.moments.append([Channel((q,), channels.depolarize(depol), "depolarize") for q in range(n)])
+    for l in range(layers):
+        for key in "ABCD":
+            if not pat[key]:
+                continue
+            c.moments.append([SweepGate((a, b), [zz_phase(gammas[s][l]) for s in range(S)], "ZZ(gamma)")
+                              for a, b in pat[key]])
+            if depol > 0:
+                c.moments.append([Channel((q,), channels.depolarize(depol), "depolarize")
+                                  for a, b in pat[key] for q in (a, b)])
+        c.moments.append([SweepGate((q,), [x_mixer(betas[s][l]) for s in range(S)], "X(beta)") for q in range(n)])
+        if depol > 0:
+            c.moments.append([Channel((q,), channels.depolarize(depol), "depolarize") for q in range(n)])
+        if amp_damp > 0:
+            c.moments.append([Channel((q,), channels.amplitude_damp(amp_damp), "amplitude_damp")
+                              for q in range(n)])
+    edges = [e for key in "ABCD" for e in pat[key]]
+    c.observables = ["".join("Z" if q in e else "I" for q in range(n)) for e in edges]
     return c
