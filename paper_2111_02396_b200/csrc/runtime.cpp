@@ -982,3 +982,87 @@ qt_status qt_expectation_partials(qt_ctx ctx, const void* state_dev, int n, int 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Diagnostics (not in the header): shared-memory wavefronts per warp store /
+// load instruction that the planner's tensor-core layouts imply for trajectory
+// `traj` (half-warp model of 8-byte accesses: 16 lanes, 16 bank pairs).
+// out[0] = chained readout store instructions (per warp), out[1] = their
+// wavefronts, out[2] = run-start fp32 gather loads, out[3] = their wavefronts,
+// out[4] = run-end fp32 stores, out[5] = their wavefronts.
+// ---------------------------------------------------------------------------
+namespace {
+uint32_t swz_h(uint32_t L) { return L ^ (((L >> 4) ^ (L >> 8)) & 15u); }
+int halfwarp_wavefronts(const uint32_t* addr32) {
+    int w = 0;
+    for (int h = 0; h < 2; ++h) {
+        int cnt[16] = {0};
+        int mx = 0;
+        for (int l = 0; l < 16; ++l) mx = std::max(mx, ++cnt[(addr32[16 * h + l] >> 3) & 15u]);
+        w += mx;
+    }
+    return w;
+}
+}  // namespace
+
+extern "C" qt_status qt_plan_bank_stats(qt_plan plan, uint64_t seed, uint64_t traj, double* out) {
+    if (!plan || !out) return fail(QT_EINVAL, "NULL argument");
+    const Plan& P = plan_of(plan);
+    ObsGroups og;
+    og.ranges.push_back({0, 0});
+    og.masks.push_back(0);
+    TrajProgram pg;
+    qt_status e = plan_trajectory(P, seed, traj, og, pg);
+    if (e != QT_OK) return e;
+    for (int i = 0; i < 6; ++i) out[i] = 0;
+    const int T = P.T;
+    auto fp32_addrs = [&](const GateDesc& G, int warp, int g, int c, uint32_t* a) {
+        for (int l = 0; l < 32; ++l) {
+            const uint32_t tid = (uint32_t)(warp * 32 + l);
+            uint32_t tb = 0;
+            for (int i = 0; i < T - 5; ++i) tb |= ((tid >> i) & 1u) << ((G.tpos >> (4 * i)) & 15u);
+            uint32_t L = tb;
+            for (int m = 0; m < 4; ++m)
+                if ((c >> m) & 1) L ^= 1u << ((G.rpos >> (4 * m)) & 15u);
+            if (g) L ^= 1u << ((G.rpos >> 16) & 15u);
+            a[l] = swz_h(L) << 3;
+        }
+    };
+    for (const PassDesc& ps : pg.passes) {
+        for (int gi = 0; gi < ps.gate_count; ++gi) {
+            const GateDesc& G = pg.gates[ps.gate_begin + gi];
+            if (!(G.k & kGateF16)) continue;
+            const bool start = (G.k & kGateRunStart) != 0 || gi == 0 || !(pg.gates[ps.gate_begin + gi - 1].k & kGateF16);
+            const bool chained = gi + 1 < ps.gate_count &&
+                                 (pg.gates[ps.gate_begin + gi + 1].k & (kGateF16 | kGateRunStart)) == kGateF16;
+            uint32_t a[32];
+            for (int warp = 0; warp < 4; ++warp)
+                for (int g = 0; g < 2; ++g)
+                    for (int c = 0; c < 16; ++c) {
+                        if (start) {
+                            fp32_addrs(G, warp, g, c, a);
+                            out[2] += 1;
+                            out[3] += halfwarp_wavefronts(a);
+                        }
+                        if (chained) {
+                            for (int l = 0; l < 32; ++l) {
+                                const uint32_t tid = (uint32_t)(warp * 32 + l);
+                                uint32_t o = 0;
+                                for (int i = 0; i < 7; ++i)
+                                    if ((tid >> i) & 1u) o ^= G.xu[5 + i];
+                                for (int m = 0; m < 4; ++m)
+                                    if ((c >> m) & 1) o ^= G.xu[m];
+                                a[l] = o;
+                            }
+                            out[0] += 1;
+                            out[1] += halfwarp_wavefronts(a);
+                        } else {
+                            fp32_addrs(G, warp, g, c, a);
+                            out[4] += 1;
+                            out[5] += halfwarp_wavefronts(a);
+                        }
+                    }
+        }
+    }
+    return QT_OK;
+}
