@@ -3,14 +3,17 @@
 Workload: 20-qubit Sycamore-style random circuit, 14 cycles,
 approximate QCS noise model (decay/dephasing triple on every qubit after every
 moment, 1q/2q depolarizing after gates, fSim coherent errors, readout errors),
-10^4 trajectories per step split over N ranks (trajectory t on rank t mod N),
+10^4 trajectories per GPU per step (rank r of N runs trajectories r + N j,
+j < 10^4: the job's trajectory indices interleave over the ranks),
 1 shot per trajectory + <Z_q> for every qubit.  Synthetic, seeded inputs.
 
-A step = one pass of the whole hot path over the 10^4 trajectories: Alg. 2
+A step = one pass of the whole hot path over each rank's 10^4 trajectories: Alg. 2
 draws + delayed-inner-product classification + fusion (host, overlapped),
 fused tile passes with on-device rho_Q/choose (K1/K2), block sums,
 observables (K4), chain-rule sampling + readout (K3), records to the host.
-Strong scaling: the total (10^4) is fixed as N grows.
+Weak scaling (trajectories are independent units, no data-path
+collective; one all-reduce of observable sums per step): per-GPU work is fixed,
+value = N * 10^4 trajectories / step time (max over ranks).
 
 `python bench.py --impl reference` times the CPU oracle (plain fp64 C, one
 trajectory per host core) on the same workload: the reference arm of this tier.
@@ -103,8 +106,7 @@ def rank_env():
 
 
 def my_share(rank, world):
-    count = (TOTAL_TRAJ - rank + world - 1) // world
-    return rank, world, count  # traj_begin, stride, count
+    return rank, world, TOTAL_TRAJ  # traj_begin, stride, count (weak scaling: 10^4 per rank)
 
 
 def run_oracle_sample(circ, seed, count, begin, stride, threads):
@@ -134,7 +136,7 @@ def bench_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded C2 generator)",
         "config": {"workload": "C2 20q sycamore-grid depth14 QCS-noise", "trajectories_per_step": per_step,
                    "l2": "n/a (CPU)"},
@@ -240,7 +242,7 @@ def bench_gpu(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     tot_ms = float(t.item())
-    value = TOTAL_TRAJ * args.steps / (tot_ms / 1e3)
+    value = world * TOTAL_TRAJ * args.steps / (tot_ms / 1e3)
 
     # ---- e2e: host circuit arrays -> C ABI (upload, fuse, run) -> host results
     e2e_times = []
@@ -263,7 +265,7 @@ def bench_gpu(args):
     te = torch.tensor([float(np.mean(e2e_times))], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = TOTAL_TRAJ / (float(te.item()) / 1e3)
+    e2e_value = world * TOTAL_TRAJ / (float(te.item()) / 1e3)
     st0 = stats[-1]
     h2d = circuit_bytes(circ) + st0["h2d_bytes"]  # circuit upload + plan tables + trajectory programs
     d2h = st0["d2h_bytes"]                        # bitstrings, Kraus records, observables, status
@@ -332,9 +334,10 @@ def bench_gpu(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32 (complex64 state; fp64 reductions)",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (complex64 state; fp64 reductions)",
             "data": "synthetic (seeded C2 generator; SURVEY 8(d))",
-            "config": {"workload": "C2 20q sycamore-grid depth14 QCS-noise", "trajectories_per_step": TOTAL_TRAJ,
+            "config": {"workload": "C2 20q sycamore-grid depth14 QCS-noise",
+                       "trajectories_per_step": TOTAL_TRAJ * world, "trajectories_per_gpu": TOTAL_TRAJ,
                        "n_qubits": N_QUBITS, "max_fused": args.fuse, "tile_bits": 12, "batch": batch,
                        "shots_per_traj": 1, "observables": len(obs), "parallelism": f"traj{world}",
                        "l2": "flushed between timed steps (512 MB write)"},
