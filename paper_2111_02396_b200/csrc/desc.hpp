@@ -11,6 +11,7 @@ enum : int32_t {
     kPassRho = 2,     // epilogue: rho_Q partial of a conventional channel + choose
     kPassFinal = 4,   // epilogue: block sums |psi|^2 (tile = low T qubits) for the sampler/norm
     kPassObs = 8,     // epilogue: Pauli-string partial sums
+    kPassInit = 16,   // the tile starts as |0...0> (first pass of a trajectory): no HBM load, always stores
 };
 
 // One tile pass of one trajectory (Sec. III.A Alg. 1 generalized: every CTA

@@ -310,7 +310,15 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
         TrajProgram& pg = progs[b];
         h_ps[b] = (int32_t)bp;
         h_pc[b] = (int32_t)pg.passes.size();
-        for (auto pd : pg.passes) {
+        double alg_adj = 0.0;
+        for (size_t pi = 0; pi < pg.passes.size(); ++pi) {
+            PassDesc pd = pg.passes[pi];
+            if (pi == 0) {
+                // the trajectory's first pass builds |0...0> in shared memory instead
+                // of loading a zeroed state (no memset, no read; it always stores)
+                if (pd.flags & kPassStore) alg_adj -= std::ldexp(1.0, n + 3);
+                pd.flags |= kPassInit | kPassStore;
+            }
             pd.gate_begin += (int32_t)bg;
             if (pd.event >= 0) pd.event += (int32_t)be;
             h_pass[bp++] = pd;
@@ -340,7 +348,7 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
             st->reductions += pg.events.size();
             st->channels_deferred += pg.n_deferred;
             st->channels_conventional += pg.n_conventional;
-            st->alg_bytes += pg.alg_bytes;
+            st->alg_bytes += pg.alg_bytes + alg_adj;
             st->alg_flops += pg.alg_flops;
         }
     }
@@ -398,9 +406,8 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
     if (!B.prepared) QT_CK(cudaEventCreateWithFlags(&B.prepared, cudaEventDisableTiming));
     QT_CK(cudaEventRecord(B.prepared, ps));
     QT_CK(cudaStreamWaitEvent(s, B.prepared, 0));
-    // |0...0> in every slot (the shared state buffer: stream-ordered after the previous batch)
-    QT_CK(launch_init_states(state, n, nslots, s));
-    uint64_t launches = 1 + (nf > 0);
+    // |0...0> in every slot: built by the first pass of each trajectory (kPassInit)
+    uint64_t launches = (nf > 0);
     TileArgs A;
     A.state = state;
     A.n = n;

@@ -662,7 +662,13 @@ tile_pass_kernel(const TileArgs A, const int step) {
     // of HBM peak vs 68% for async copies at n = 30).  hoff and swz are linear in
     // the index bits: slot L = tid + m NT has global offset hoff[tid >> CL] +
     // hoff[m NT >> CL] + (tid & (2^CL - 1)) (NT >= 2^CL).
-    if constexpr (NT >= (1 << CL)) {
+    if (P.flags & kPassInit) {
+        // first pass of a trajectory: the tile of |0...0> (amplitude 0 = 1 lives in
+        // tile 0 at slot swz(0) = 0), no HBM load
+        float4* t4 = reinterpret_cast<float4*>(tile);
+        for (int i = tid; i < (1 << T) / 2; i += NT) t4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (tid == 0 && blockIdx.x == 0) t4[0] = make_float4(1.f, 0.f, 0.f, 0.f);
+    } else if constexpr (NT >= (1 << CL)) {
         const float2* gsrc = st + base + hoff[tid >> CL] + ((uint32_t)tid & ((1u << CL) - 1u));
         const uint32_t sb = swz((uint32_t)tid);
 #pragma unroll 8
