@@ -369,7 +369,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--fuse", type=int, default=4)
     ap.add_argument("--tensor-cores", type=int, default=0, help="0 auto, 1 on, -1 CUDA-core K1")
-    ap.add_argument("--batch", type=int, default=128)
+    ap.add_argument("--batch", type=int, default=384)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sweep-n", type=int, default=30, help="qubits of the gate-pass bandwidth sweep (0 = skip)")
     args = ap.parse_args()

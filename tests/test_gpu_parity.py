@@ -229,6 +229,30 @@ def test_config2_sample_of_trajectories(ctx):
     compare(ref, out, state)
 
 
+def test_config2_full_batch_launch(ctx):
+    """C2 in bench.py's launch configuration: one full batch of 384 slots (3 GiB of
+    state, byte offsets past 2^31), trajectories t = 17 + 26 j; slots 0, 127, 255
+    and 383 are checked against the oracle one by one, and every slot's records
+    are a valid Kraus index with a normalised state."""
+    c = workloads.sycamore_grid_qcs(config=2)
+    seed = workloads.trajectory_seed(2)
+    B = 384
+    plan = qtraj.Plan(qtraj.Circuit.from_description(c), max_fused=4)
+    state = torch.zeros(B << 20, dtype=torch.complex64, device="cuda")
+    out = ctx.run_trajectories(plan, state, seed=seed, traj_count=B, traj_begin=17, traj_stride=26, batch=B,
+                               shots=1, observables=c.observables)
+    torch.cuda.synchronize()
+    kmax = np.array([len(op.kraus) for op in c.ops() if hasattr(op, "kraus")])
+    assert np.all((out["kraus"] >= 0) & (out["kraus"] < kmax[None, :]))
+    norms = torch.linalg.vector_norm(state.view(B, -1), dim=1).cpu().numpy()
+    assert np.all(np.isfinite(norms)) and np.all(norms > 0)
+    for j in (0, 127, 255, 383):
+        ref = oracle.run_trajectories(c, seed=seed, traj_begin=17 + 26 * j, traj_count=1, shots=1,
+                                      want_states=True)
+        sub = {"kraus": out["kraus"][j:j + 1], "bits": out["bits"][j:j + 1], "obs": out["obs"][j:j + 1]}
+        compare(ref, sub, state.view(B, -1)[j], check_states=True)
+
+
 # ---------------------------------------------------------------------------
 # K1 f16 tensor-core runs: the tile scale (DESIGN R11) under norm growth,
 # tiny amplitudes and all-zero tiles; chains of 4-qubit operators applied with
