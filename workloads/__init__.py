@@ -309,9 +309,12 @@ def sycamore_grid_qcs(rows: int = 4, cols: int = 5, cycles: int = 14,
 
 
 def low_noise_grid(rows: int = 2, cols: int = 13, cycles: int = 20, config: int = 3,
-                   depol: float = 1e-3, gamma_pd: float = 1e-4) -> Circuit:
+                   depol: float = 1e-3, gamma_pd: float = 1e-4, damping: str = "phase") -> Circuit:
     """C3: depolarize(1e-3) after every gate (unitary mixture, always deferred)
-    plus phase_damp(gamma) on every qubit per moment."""
+    plus phase_damp(gamma) on every qubit per moment.
+    damping="amplitude": amplitude_damp(gamma) instead (C4 (ii): 4 x 8 grid,
+    depolarize 1e-3, gamma = 1e-4)."""
+    damp = channels.phase_damp if damping == "phase" else channels.amplitude_damp
     rng = np.random.default_rng(circuit_seed(config))
     n = rows * cols
     c = Circuit(n)
@@ -330,12 +333,12 @@ def low_noise_grid(rows: int = 2, cols: int = 13, cycles: int = 20, config: int 
         c.moments.append(m1)
         if depol > 0:
             c.moments.append([Channel((q,), channels.depolarize(depol)) for q in range(n)])
-        c.moments.append([Channel((q,), channels.phase_damp(gamma_pd)) for q in range(n)])
+        c.moments.append([Channel((q,), damp(gamma_pd)) for q in range(n)])
         pairs = pats[order[cyc % len(order)]]
         c.moments.append([Gate(pr, fsim, "fSim") for pr in pairs])
         if depol > 0:
             c.moments.append([Channel(pr, channels.depolarize2(depol)) for pr in pairs])
-        c.moments.append([Channel((q,), channels.phase_damp(gamma_pd)) for q in range(n)])
+        c.moments.append([Channel((q,), damp(gamma_pd)) for q in range(n)])
     c.observables = ["I" * q + "Z" + "I" * (n - q - 1) for q in range(n)]
     return c
 
