@@ -317,9 +317,68 @@ unsigned bank_vec(const GateDesc* nx, int b) {
 // half-warp's lanes) get tile bits whose bank vectors in the output layout are
 // linearly independent, so the half-warp's 8-byte stores of one configuration
 // hit 16 distinct bank pairs; the group bit is the highest remaining tile bit.
-void tc_relayout(GateDesc& gd, const GateDesc* nx, int T, int grp) {
+// GF(2) rank of up to 4 bank vectors (4-bit).
+int rank4(const unsigned* v, int count) {
+    unsigned basis[4] = {0, 0, 0, 0};
+    int r = 0;
+    for (int i = 0; i < count; ++i) {
+        unsigned x = v[i];
+        for (int j = 3; j >= 0 && x; --j)
+            if ((x >> j) & 1u) {
+                if (!basis[j]) {
+                    basis[j] = x;
+                    ++r;
+                    break;
+                }
+                x ^= basis[j];
+            }
+    }
+    return r;
+}
+
+// run_start: the gate also gathers the fp32 tile in its layout at the start of
+// the run (8-byte loads, bank vector of tile bit b = 2^(b mod 4) under the
+// tile swizzle), so the four lane bits are chosen among all subsets of the
+// free tile bits: full rank for the stores first, then for the gather.
+void tc_relayout(GateDesc& gd, const GateDesc* nx, int T, int grp, bool run_start = false) {
     uint32_t cfg = 0;
     for (int m = 0; m < 4; ++m) cfg |= 1u << ((gd.rpos >> (4 * m)) & 15u);
+    if (run_start) {
+        int cand[12], nc = 0;
+        for (int b = 0; b < T; ++b)
+            if (!(((cfg | (1u << grp)) >> b) & 1u)) cand[nc++] = b;
+        int best[4] = {-1, -1, -1, -1}, best_score = -1;
+        for (int a = 0; a < nc; ++a)
+            for (int b = a + 1; b < nc; ++b)
+                for (int c = b + 1; c < nc; ++c)
+                    for (int d = c + 1; d < nc; ++d) {
+                        const int pick[4] = {cand[a], cand[b], cand[c], cand[d]};
+                        unsigned vs[4], vg[4];
+                        for (int i = 0; i < 4; ++i) {
+                            vs[i] = bank_vec(nx, pick[i]);
+                            vg[i] = 1u << (pick[i] & 3);
+                        }
+                        const int score = 8 * rank4(vs, 4) + rank4(vg, 4);
+                        if (score > best_score) {
+                            best_score = score;
+                            for (int i = 0; i < 4; ++i) best[i] = pick[i];
+                        }
+                    }
+        if (best_score >= 0) {
+            int lanes[12], nl = 0;
+            uint32_t used = cfg | (1u << grp);
+            for (int i = 0; i < 4; ++i) {
+                lanes[nl++] = best[i];
+                used |= 1u << best[i];
+            }
+            for (int b = 0; b < T; ++b)
+                if (!((used >> b) & 1u)) lanes[nl++] = b;
+            gd.rpos = (gd.rpos & 0xffffu) | ((uint32_t)grp << 16);
+            gd.tpos = 0;
+            for (int i = 0; i < nl; ++i) gd.tpos |= (uint32_t)lanes[i] << (4 * i);
+            return;
+        }
+    }
     int lanes[12], nl = 0;
     unsigned basis[4] = {0, 0, 0, 0};  // GF(2) basis by leading bit
     uint32_t used = cfg | (1u << grp);
@@ -398,7 +457,8 @@ void tc_runs(GateDesc* gd, const double* norms, int count, int T) {
         g = e + 1;
     }
     for (int g = count - 1; g >= 0; --g)
-        if (gd[g].k & kGateF16) tc_relayout(gd[g], chained(g) ? &gd[g + 1] : nullptr, T, grp[g]);
+        if (gd[g].k & kGateF16)
+            tc_relayout(gd[g], chained(g) ? &gd[g + 1] : nullptr, T, grp[g], !(g > 0 && chained(g - 1)));
     for (int g = 0; g < count; ++g) {
         if (!chained(g)) continue;
         for (int r = 0; r < 12; ++r) {
