@@ -207,9 +207,15 @@ def bench_gpu(args):
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream(dev)
 
+    # host planning threads: the node's cores split over the ranks on it (no oversubscription)
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    host_threads = max(1, (len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else
+                           (os.cpu_count() or 1)) // max(local_world, 1))
+
     def step(profile):
         out = ctx.run_trajectories(plan, state, seed=seed, traj_count=count, traj_begin=begin, traj_stride=stride,
-                                   shots=1, batch=batch, observables=obs, profile=profile)
+                                   shots=1, batch=batch, observables=obs, profile=profile,
+                                   host_threads=host_threads)
         # job output: per-observable sums over this rank's trajectories, reduced over ranks
         sums = torch.tensor(np.concatenate([out["obs"].sum(0), (out["obs"] ** 2).sum(0)]), device=dev,
                             dtype=torch.float64)
@@ -256,7 +262,7 @@ def bench_gpu(args):
         e0.record(stream)
         c2, plan2 = build_plan(circ, args.fuse)
         o2 = ctx.run_trajectories(plan2, state, seed=seed, traj_count=count, traj_begin=begin, traj_stride=stride,
-                                  shots=1, batch=batch, observables=obs)
+                                  shots=1, batch=batch, observables=obs, host_threads=host_threads)
         mean = o2["obs"].mean(0)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -354,6 +360,7 @@ def bench_gpu(args):
                        "trajectories_per_step": TOTAL_TRAJ * world, "trajectories_per_gpu": TOTAL_TRAJ,
                        "n_qubits": N_QUBITS, "max_fused": args.fuse, "tile_bits": 12, "batch": batch,
                        "shots_per_traj": 1, "observables": len(obs), "parallelism": f"traj{world}",
+                       "host_threads_per_rank": host_threads,
                        "l2": "flushed between timed steps (512 MB write)"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(sum(s["launches"] for s in stats)),
