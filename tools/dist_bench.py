@@ -3,6 +3,7 @@ noiseless or amplitude damping gamma = 1e-3 per qubit per moment).
 
   torchrun --nproc-per-node N tools/dist_bench.py --n-local 33    # C5: 36 q on 8 GPUs
   python tools/dist_bench.py --emulate 8 --n-local 26             # one GPU, 8 virtual ranks
+  python tools/dist_bench.py --emulate 8 --n-local 30 --mirror    # 33 q: C then C^dag -> |0...0>
 
 Prints one JSON line (rank 0): seconds per trajectory, swaps, exchanged bytes."""
 import argparse
@@ -44,6 +45,8 @@ def main():
     ap.add_argument("--cycles", type=int, default=10)
     ap.add_argument("--gamma", type=float, default=0.0)
     ap.add_argument("--traj", type=int, default=1)
+    ap.add_argument("--mirror", action="store_true",
+                    help="noiseless C then C^dag: every sample must be 0...0 and every <Z_q> = 1")
     a = ap.parse_args()
     if a.emulate:
         world, rank, local = a.emulate, 0, 0
@@ -59,14 +62,22 @@ def main():
     n = a.n_local + g
     ctx = qtraj.Context(local)
     backend = D.GpuBackend(ctx, torch.device("cuda", local))
-    c = c5_circuit(n, a.cycles, a.gamma)
+    c = c5_circuit(n, a.cycles, 0.0 if a.mirror else a.gamma)
+    if a.mirror:
+        inv = [[workloads.Gate(op.qubits, np.conj(np.asarray(op.matrix)).T) for op in m] for m in reversed(c.moments)]
+        c.moments = c.moments + inv
+        c.observables = ["I" * q + "Z" + "I" * (n - q - 1) for q in (0, n // 2, n - 1)]
+    shots = 16 if a.mirror else 1
+    mirror_ok = True
     times, swaps, xbytes = [], [], []
     for t in range(a.traj + 1):  # trajectory 0 = warm-up
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         tr = D.DistributedTrajectory(backend, fabric, n)
-        out = tr.run(c, seed=workloads.trajectory_seed(5), traj=t, shots=1)
+        out = tr.run(c, seed=workloads.trajectory_seed(5), traj=t, shots=shots, observables=c.observables)
         torch.cuda.synchronize()
+        if a.mirror:
+            mirror_ok &= bool(np.all(out["bits"] == 0)) and bool(np.allclose(out["obs"], 1.0, atol=1e-4))
         if t:
             times.append(time.perf_counter() - t0)
             swaps.append(out["swaps"])
@@ -76,7 +87,8 @@ def main():
         print(json.dumps({"mode": "emulated" if a.emulate else "nccl", "world": world, "n": n, "n_local": a.n_local,
                           "cycles": a.cycles, "gamma": a.gamma, "ops": sum(1 for _ in c.ops()),
                           "s_per_traj": float(np.mean(times)), "swaps_per_traj": float(np.mean(swaps)),
-                          "exchanged_GB_per_rank": float(np.mean(xbytes)) / 1e9 / max(1, len(fabric.local_ranks))}),
+                          "exchanged_GB_per_rank": float(np.mean(xbytes)) / 1e9 / max(1, len(fabric.local_ranks)),
+                          **({"mirror_all_zero_and_Z_1": mirror_ok} if a.mirror else {})}),
               flush=True)
 
 
