@@ -513,31 +513,36 @@ __device__ __forceinline__ void apply_tc_wide(float2* tile, unsigned char* wbuf,
         // row t holds (hi or lo part) x W_hi in columns [0, 128) and x W_lo in
         // [128, 256); output column n = 2 j + b.  Thread t keeps the outputs of its
         // configuration half (columns 64 h ..) and sends the other half to t ^ 64.
+        // Rows t >= 64 (warps 2, 3) hold lo parts: their x_lo W_lo columns are the
+        // dropped fourth product (as for k <= 5), so those warps read only x_lo W_hi
+        // (a quarter less TMEM traffic; tcgen05.ld stays warp-uniform).
         float* xbuf = reinterpret_cast<float*>(wbuf);
         const uint32_t sh = 64u * (h ^ 1u), kh = 64u * h;
+        const bool lo_row = h != 0u;
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
             uint32_t a[32], b[32];
             tmem_ld32(tmem + lane_off + sh + 32 * p, a);
-            tmem_ld32(tmem + lane_off + 128 + sh + 32 * p, b);
+            if (!lo_row) tmem_ld32(tmem + lane_off + 128 + sh + 32 * p, b);
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-                xbuf[(32 * p + i) * 128 + (tid ^ 64u)] = __uint_as_float(a[i]) + __uint_as_float(b[i]);
+                xbuf[(32 * p + i) * 128 + (tid ^ 64u)] =
+                    lo_row ? __uint_as_float(a[i]) : __uint_as_float(a[i]) + __uint_as_float(b[i]);
         }
         __syncthreads();
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
             uint32_t a[32], b[32];
             tmem_ld32(tmem + lane_off + kh + 32 * p, a);
-            tmem_ld32(tmem + lane_off + 128 + kh + 32 * p, b);
+            if (!lo_row) tmem_ld32(tmem + lane_off + 128 + kh + 32 * p, b);
             tmem_wait_ld();
 #pragma unroll
             for (int c = 0; c < 16; ++c) {
-                const float yr = (__uint_as_float(a[2 * c]) + __uint_as_float(b[2 * c])) +
-                                 xbuf[(32 * p + 2 * c) * 128 + tid];
-                const float yi = (__uint_as_float(a[2 * c + 1]) + __uint_as_float(b[2 * c + 1])) +
-                                 xbuf[(32 * p + 2 * c + 1) * 128 + tid];
+                const float ar = __uint_as_float(a[2 * c]), ai = __uint_as_float(a[2 * c + 1]);
+                const float yr = (lo_row ? ar : ar + __uint_as_float(b[2 * c])) + xbuf[(32 * p + 2 * c) * 128 + tid];
+                const float yi =
+                    (lo_row ? ai : ai + __uint_as_float(b[2 * c + 1])) + xbuf[(32 * p + 2 * c + 1) * 128 + tid];
                 *reinterpret_cast<float2*>(tb8 + (base ^ lo[16 * p + c])) = upk2(mul2(pk2(yr, yi), inv2));
             }
         }

@@ -48,6 +48,8 @@ if @CHAIN@:
 if @SWEEP@:
     s = bench.gate_pass_sweep(ctx, 30, torch.device("cuda", 0), 6554.9)
     print(@LIB@, "sweep", {k: v for k, v in s.items() if "frac" in k or k == "gbps"}, flush=True)
+    print(@LIB@, "sweep k=5,6", [(r["k"], r["placement"], round(r["frac"], 3)) for r in s["rows"] if r["k"] >= 5],
+          flush=True)
 '''
 sweep = "--sweep" in sys.argv
 chain = "--chain" in sys.argv
