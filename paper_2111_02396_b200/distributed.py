@@ -162,6 +162,9 @@ class TorchFabric:
         self.device = device
 
     def exchange_top(self, states, gbits, s, pool=None):
+        # chunk c goes to rank _dest(c) and arrives at chunk _src_chunk(source):
+        # both are increasing in rank order only for ascending gbits
+        assert all(gbits[j] < gbits[j + 1] for j in range(len(gbits) - 1)), "gbits must ascend"
         x = states[self.rank]
         chunk = x.numel() >> s
         in_split = [0] * self.world
@@ -311,6 +314,12 @@ class DistributedTrajectory:
         """Exchange logical qubits `glob` (global) with `victims` (local)."""
         s = len(glob)
         assert len(victims) == s
+        # pair j <-> rank bit gbits[j] in ascending order: the all-to-all then sends
+        # chunk c to ranks in increasing order and receives chunks in source-rank
+        # order (TorchFabric relies on it)
+        pairs = sorted(zip(glob, victims), key=lambda gv: self.slot[gv[0]])
+        glob = [g for g, _ in pairs]
+        victims = [v for _, v in pairs]
         self._flush()
         # local permutation: victim j -> top slot nl - s + j (swapping with the occupant)
         top = [self.nl - s + j for j in range(s)]
@@ -364,9 +373,29 @@ class DistributedTrajectory:
         return out, pos
 
     def _ensure_local(self, qubits: Sequence[int], upcoming: List[set]):
+        """Make `qubits` local.  The all-to-all of an s-qubit swap moves (1 - 2^-s) of
+        the state, so other global qubits ride along when they are used (within the
+        lookahead) before the local victim that would replace them (Belady): one
+        3-qubit exchange (7/8 of the state) instead of three 1-qubit ones (3/2)."""
         glob = [q for q in qubits if self.slot[q] >= self.nl]
-        if glob:
-            self._swap_in(glob, self._choose_victims(len(glob), set(qubits), upcoming))
+        if not glob:
+            return
+
+        def next_use(q):
+            for i, ops in enumerate(upcoming):
+                if q in ops:
+                    return i
+            return 1 << 30
+        others = sorted((q for q in range(self.n) if self.slot[q] >= self.nl and q not in glob), key=next_use)
+        victims = self._choose_victims(len(glob) + len(others), set(qubits), upcoming)
+        take, vict = list(glob), victims[:len(glob)]
+        for j, x in enumerate(others):
+            k = len(glob) + j
+            if k >= len(victims) or not next_use(x) < min(next_use(victims[k]), len(upcoming)):
+                break
+            take.append(x)
+            vict.append(victims[k])
+        self._swap_in(take, vict)
 
     # -- Alg. 2 over a distributed register ---------------------------------
     def run(self, circuit, seed: int, traj: int, shots: int = 1, observables: Sequence[str] = (),

@@ -138,15 +138,20 @@ def _free_port():
     return p
 
 
-def _gloo_worker(rank, port, q):
+def _gloo_n(world):
+    return max(8, 6 + world.bit_length() - 1)  # >= 6 local qubits per rank
+
+
+def _gloo_worker(rank, port, q, world=2):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=2)
-    c = circuit(8, seed=6)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = _gloo_n(world)
+    c = circuit(n, seed=6)
     res = []
     for t in range(2):
-        tr = D.DistributedTrajectory(NumpyBackend(), D.TorchFabric(), 8)
+        tr = D.DistributedTrajectory(NumpyBackend(), D.TorchFabric(), n)
         out = tr.run(c, seed=77, traj=t, shots=2, observables=c.observables)
         res.append({k: np.asarray(v) for k, v in out.items() if k in ("kraus", "bits", "obs")})
     q.put((rank, res))
@@ -154,21 +159,25 @@ def _gloo_worker(rank, port, q):
     dist.destroy_process_group()
 
 
-def test_two_rank_gloo_distributed_state_matches_oracle():
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_gloo_distributed_state_matches_oracle(world):
+    """torch.distributed (gloo) all-to-all exchanges; worlds 4 and 8 have 2 and 3
+    global qubits, so multi-qubit exchanges (ride-along swaps) run through
+    TorchFabric (the 8-GPU C5 layout)."""
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_gloo_worker, args=(r, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=_gloo_worker, args=(r, port, q, world)) for r in range(world)]
     for p in ps:
         p.start()
-    got = dict(q.get(timeout=300) for _ in range(2))
+    got = dict(q.get(timeout=240) for _ in range(world))
     for p in ps:
         p.join(timeout=120)
         assert p.exitcode == 0
-    c = circuit(8, seed=6)
+    c = circuit(_gloo_n(world), seed=6)
     ref = oracle.run_trajectories(c, seed=77, traj_count=2, shots=2)
-    for rank in (0, 1):
+    for rank in range(world):
         for t in range(2):
             check(got[rank][t], ref, t)
 
