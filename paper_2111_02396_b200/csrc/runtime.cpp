@@ -996,7 +996,9 @@ qt_status qt_expectation_partials(qt_ctx ctx, const void* state_dev, int n, int 
 // `traj` (half-warp model of 8-byte accesses: 16 lanes, 16 bank pairs).
 // out[0] = chained readout store instructions (per warp), out[1] = their
 // wavefronts, out[2] = run-start fp32 gather loads, out[3] = their wavefronts,
-// out[4] = run-end fp32 stores, out[5] = their wavefronts.
+// out[4] = run-end fp32 stores, out[5] = their wavefronts, out[6] = chained
+// transitions, out[7] = those whose next gate uses another group bit (no
+// two-group overlap).  `out` holds 8 doubles.
 // ---------------------------------------------------------------------------
 namespace {
 uint32_t swz_h(uint32_t L) { return L ^ (((L >> 4) ^ (L >> 8)) & 15u); }
@@ -1021,7 +1023,7 @@ extern "C" qt_status qt_plan_bank_stats(qt_plan plan, uint64_t seed, uint64_t tr
     TrajProgram pg;
     qt_status e = plan_trajectory(P, seed, traj, og, pg);
     if (e != QT_OK) return e;
-    for (int i = 0; i < 6; ++i) out[i] = 0;
+    for (int i = 0; i < 8; ++i) out[i] = 0;
     const int T = P.T;
     auto fp32_addrs = [&](const GateDesc& G, int warp, int g, int c, uint32_t* a) {
         for (int l = 0; l < 32; ++l) {
@@ -1042,6 +1044,10 @@ extern "C" qt_status qt_plan_bank_stats(qt_plan plan, uint64_t seed, uint64_t tr
             const bool start = (G.k & kGateRunStart) != 0 || gi == 0 || !(pg.gates[ps.gate_begin + gi - 1].k & kGateF16);
             const bool chained = gi + 1 < ps.gate_count &&
                                  (pg.gates[ps.gate_begin + gi + 1].k & (kGateF16 | kGateRunStart)) == kGateF16;
+            if (chained) {
+                out[6] += 1;
+                out[7] += G.xu[4] != (uint16_t)16384;  // tc::kF16GroupBytes
+            }
             uint32_t a[32];
             for (int warp = 0; warp < 4; ++warp)
                 for (int g = 0; g < 2; ++g)
