@@ -423,11 +423,8 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
     if (P.T == 12) {
         P.R = std::max(f <= 4 ? 4 : f, max_arity);
     } else {
-        P.R = std::min(P.T, 4);
-        if (max_arity > P.R) {
-            delete hp;
-            return fail(QT_EARITY, "operations on more than 4 qubits need n >= 12 in this build");
-        }
+        // whole-state tiles (n < 12): 2^R amplitudes per thread hold the widest gate
+        P.R = std::min(P.T, std::max(4, std::max(max_arity, f)));
     }
     P.f = std::min(f, P.R);
     P.one_gate = o.one_gate_per_pass != 0;

@@ -33,6 +33,9 @@ namespace qt {
 // Tile-pass instantiations live in tile_pass_{r4,r5,r6,tc}.cu (parallel compile).
 cudaError_t launch_tile_pass_r4(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s);
 cudaError_t launch_tile_pass_r5(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s);
+cudaError_t launch_tile_pass_r5s(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s);
+cudaError_t launch_tile_pass_r6s_a(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s);
+cudaError_t launch_tile_pass_r6s_b(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s);
 cudaError_t launch_tile_pass_r6(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s);
 cudaError_t launch_tile_pass_tc(const TileArgs& a, int tck, int step, uint32_t ntiles, int nslots, cudaStream_t s);
 
@@ -40,12 +43,16 @@ size_t tile_pass_smem_bytes(int T, int R, int tck) { return tile_pass_smem_bytes
 
 cudaError_t launch_tile_pass(const TileArgs& a, int R, int tck, int step, uint32_t ntiles, int nslots,
                              cudaStream_t s) {
-    // Instantiated (T, R): (12, 4), (12, 5), (12, 6) and (T, min(T, 4)) for
-    // T = 1..11 (the whole state of n < 12 qubits in one CTA); tensor cores
+    // Instantiated (T, R): (12, 4), (12, 5), (12, 6), (T, min(T, 4)) for
+    // T = 1..11 (the whole state of n < 12 qubits in one CTA) and (T, 5 | 6) for
+    // T = R..11 (5- and 6-qubit gates on small registers); tensor cores
     // (tck = 4, 5 or 6 qubits per padded gate): (12, 5).
     if (tck) return a.T == 12 && R == 5 ? launch_tile_pass_tc(a, tck, step, ntiles, nslots, s) : cudaErrorInvalidValue;
     if (a.T == 12 && R == 6) return launch_tile_pass_r6(a, step, ntiles, nslots, s);
     if (a.T == 12 && R == 5) return launch_tile_pass_r5(a, step, ntiles, nslots, s);
+    if (a.T < 12 && R == 5) return launch_tile_pass_r5s(a, step, ntiles, nslots, s);
+    if (a.T < 12 && R == 6) return a.T <= 8 ? launch_tile_pass_r6s_a(a, step, ntiles, nslots, s)
+                                            : launch_tile_pass_r6s_b(a, step, ntiles, nslots, s);
     if (R == (a.T < 4 ? a.T : 4)) return launch_tile_pass_r4(a, step, ntiles, nslots, s);
     return cudaErrorInvalidValue;
 }

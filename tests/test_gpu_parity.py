@@ -61,8 +61,6 @@ def placements(n, k, rng):
 def test_apply_gate_matches_oracle(ctx, n, k):
     if k > n:
         pytest.skip()
-    if n < 12 and k > 4:
-        pytest.skip("k > 4 needs n >= 12 in this build")
     rng = np.random.default_rng(10 * n + k)
     for qs in placements(n, k, rng):
         U = workloads.haar_unitary(rng, 2 ** k)
@@ -341,6 +339,20 @@ def test_wide_fused_gates_trajectories(ctx, f, tensor_cores):
                                  t1_ns=800.0, tphi_ns=1400.0, readout=True)
     ref, out, state = run_both(ctx, c, seed=19, T=8, shots=2, f=f, tensor_cores=tensor_cores)
     compare(ref, out, state)
+
+
+@pytest.mark.parametrize("n", [6, 8, 11])
+@pytest.mark.parametrize("f", [5, 6])
+def test_wide_gates_small_registers(ctx, n, f):
+    """5- and 6-qubit operations on registers smaller than a tile (whole-state
+    tiles with 2^5 / 2^6 amplitudes per thread)."""
+    c = workloads.random_circuit(n, depth=5, seed=3 * n + f, max_arity=f, noise="both", p=0.03, t1_ns=600.0,
+                                 tphi_ns=900.0, readout=True)
+    rng = np.random.default_rng(n + f)
+    wide = tuple(int(q) for q in rng.permutation(n)[:f])  # unsorted: Kronecker order exercised
+    c.moments.insert(2, [Gate(wide, workloads.haar_unitary(rng, 2 ** f))])
+    ref, out, state = run_both(ctx, c, seed=19, T=8, shots=2, f=f)
+    assert compare(ref, out, state) == 0
 
 
 def test_tc_run_zero_tiles(ctx):
