@@ -493,9 +493,9 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
             po.mixture = mixture;
             if (!mixture) P.max_conv_d = std::max(P.max_conv_d, d);
             P.max_chan_d = std::max(P.max_chan_d, d);
-            if (!mixture && hop->nq > 2) {
+            if (!mixture && hop->nq > 3) {
                 delete hp;
-                return fail(QT_EARITY, "non-unitary-mixture channels on more than 2 qubits are not supported by the device choose step");
+                return fail(QT_EARITY, "non-unitary-mixture channels on more than 3 qubits are not supported by the device choose step");
             }
             // variants: deferred application of K_i (mixtures: K_i / sqrt(pbar_i), exactly unitary)
             for (int i = 0; i < hop->n_kraus; ++i) {

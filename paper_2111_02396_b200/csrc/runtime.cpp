@@ -373,7 +373,7 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
     QT_CK(B.pool.ensure(sizeof(float2) * std::max<int32_t>(pool, 2)));
     QT_CK(B.status.ensure(sizeof(int32_t) * nslots));
     QT_CK(B.counters.ensure(sizeof(int32_t) * nslots));
-    const int rd = std::min(P.max_chan_d, 4);  // conventional mode reduces every channel (q <= 2)
+    const int rd = std::min(P.max_chan_d, 8);  // conventional mode reduces every channel (q <= 3)
     const int rho_stride = 2 * rd * rd;
     QT_CK(B.rho_part.ensure(sizeof(double) * (size_t)nslots * ntiles * rho_stride));
     QT_CK(B.blocksum.ensure(sizeof(double) * (size_t)nslots * ntiles));
@@ -588,8 +588,8 @@ qt_status qt_run_trajectories(qt_ctx ctx, qt_plan plan, const qt_run_opts* opts,
     if (!ctx || !plan || !opts || !state_dev) return fail(QT_EINVAL, "NULL argument");
     if (n_obs < 0 || (n_obs > 0 && !obs)) return fail(QT_EINVAL, "bad observables");
     if (opts->mode != 0 && opts->mode != 1) return fail(QT_EINVAL, "mode must be 0 (delayed) or 1 (conventional)");
-    if (opts->mode == 1 && plan_of(plan).max_chan_d > 4)
-        return fail(QT_EARITY, "conventional mode reduces every channel: channels on more than 2 qubits are not supported");
+    if (opts->mode == 1 && plan_of(plan).max_chan_d > 8)
+        return fail(QT_EARITY, "conventional mode reduces every channel: channels on more than 3 qubits are not supported");
     if (opts->shots_per_traj < 0) return fail(QT_EINVAL, "shots_per_traj < 0");
     const Plan& P = plan_of(plan);
     QT_CK(cudaSetDevice(ctx->device));

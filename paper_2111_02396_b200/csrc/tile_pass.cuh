@@ -293,6 +293,40 @@ __device__ __forceinline__ void rho_partial(const float2* tile, uint32_t qlocal,
         for (int e = 0; e < 2 * D * D; ++e) out[e] = acc[e];
 }
 
+// rho_Q of a Q = 3 qubit channel (8 x 8): one row a at a time (2 D doubles per
+// thread in registers), the tile re-read per row; same summation order per entry
+// as rho_partial (slots strided over threads, then the fixed block sum).
+template <int Q, int T, int NT>
+__device__ __forceinline__ void rho_partial_rows(const float2* tile, uint32_t qlocal, double* out /*2*D*D*/,
+                                                 double* red) {
+    constexpr int D = 1 << Q;
+    const int tid = threadIdx.x;
+    uint32_t qoff[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) qoff[a] = pdep32((uint32_t)a, qlocal);
+#pragma unroll 1
+    for (int a = 0; a < D; ++a) {
+        double acc[2 * D];
+#pragma unroll
+        for (int e = 0; e < 2 * D; ++e) acc[e] = 0.0;
+        for (uint32_t bL = tid; bL < (1u << T); bL += NT) {
+            if (bL & qlocal) continue;
+            const float2 va = tile[swz(bL | qoff[a])];
+            const double ar = va.x, ai = va.y;
+#pragma unroll
+            for (int b = 0; b < D; ++b) {
+                const float2 vb = tile[swz(bL | qoff[b])];
+                acc[2 * b] += ar * (double)vb.x + ai * (double)vb.y;
+                acc[2 * b + 1] += ai * (double)vb.x - ar * (double)vb.y;
+            }
+        }
+        block_sum_n<NT, 2 * D>(acc, red);
+        if (tid == 0)
+#pragma unroll
+            for (int e = 0; e < 2 * D; ++e) out[2 * D * a + e] = acc[e];
+    }
+}
+
 // Alg. 2 lines 13-21 for one conventional channel, single thread.
 static __device__ __noinline__ void choose_conventional(const EventDesc& E, const ChanDesc& C, const double* cd,
                                     const double* rho /*2*d*d*/, float2* pool, int32_t* records,

@@ -91,6 +91,14 @@ __device__ __forceinline__ void fp32_layout(const GateDesc& G, uint32_t (&lo)[16
     base = swz(tb) << 3;
 }
 
+// 3-qubit device-chosen operators (conventional 3-qubit channels) in the tensor-core
+// kernel: an out-of-line call (unit passed through local memory).
+template <int R>
+__device__ __noinline__ void apply_fused3_outlined(float2* tile, const float2* M, uint32_t pbase,
+                                                   const uint32_t (&unit)[R]) {
+    apply_fused<3, R>(tile, M, pbase, unit);
+}
+
 // A run of tensor-core gates (4 qubits, kind::f16; tc_common.cuh), gates g0..g1
 // of the pass (returns g1).  Run start: gather the fp32 tile in the first
 // gate's layout, pick the power-of-two tile scale (max |component| -> [2^6,
@@ -748,10 +756,12 @@ tile_pass_kernel(const TileArgs A, const int step) {
                                   ph[0]);
                 else if constexpr (R == 5 && (TCK == 5 || TCK == 6))
                     apply_tc_wide<TCK>(tile, mcur, G, tmem, mbar, ph[0], red);
-            } else if ((G.k & 0xff) == 1) {  // device-chosen conventional operators (q <= 2)
+            } else if ((G.k & 0xff) == 1) {  // device-chosen conventional operators (q <= 3)
                 apply_fused<1, R>(tile, reinterpret_cast<const float2*>(mcur), swz(tb) << 3, unit);
-            } else {
+            } else if ((G.k & 0xff) == 2) {
                 apply_fused<2, R>(tile, reinterpret_cast<const float2*>(mcur), swz(tb) << 3, unit);
+            } else {  // rare: kept out of line so the tensor-core kernel's hot code is unchanged
+                apply_fused3_outlined<R>(tile, reinterpret_cast<const float2*>(mcur), swz(tb) << 3, unit);
             }
             continue;
         }
@@ -769,7 +779,11 @@ tile_pass_kernel(const TileArgs A, const int step) {
         const ChanDesc C = A.chans[E.chan];
         const uint32_t ql = to_local<T>(C.qmask, P);  // channel qubits as tile-local bits
         double* out = A.rho_part + tile_row * A.rho_stride;
-        if constexpr (T >= 2) {
+        if constexpr (T >= 3) {
+            if (C.nq == 1) rho_partial<1, T, NT>(tile, ql, out, red);
+            else if (C.nq == 2) rho_partial<2, T, NT>(tile, ql, out, red);
+            else rho_partial_rows<3, T, NT>(tile, ql, out, red);
+        } else if constexpr (T >= 2) {
             if (C.nq == 1) rho_partial<1, T, NT>(tile, ql, out, red);
             else rho_partial<2, T, NT>(tile, ql, out, red);
         } else {

@@ -131,3 +131,27 @@ def test_many_shots_per_trajectory(ctx):
     c = workloads.random_circuit(10, depth=6, seed=5, noise="depol", p=0.02, readout=True)
     ref, out, state = run_both(ctx, c, seed=21, T=3, shots=1024)
     assert compare(ref, out, state) == 0
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("n", [7, 14])
+def test_three_qubit_conventional_channels(ctx, n, mode):
+    """3-qubit non-mixture channels (products of amplitude damping, 8 Kraus
+    operators of 8 x 8): rho_Q is 8 x 8 on the device; in the conventional mode
+     a 3-qubit depolarizing channel (64 Paulis) is reduced too."""
+    rng = np.random.default_rng(n + 10 * mode)
+    ad = [np.kron(np.kron(a, b), c) for a in channels.amplitude_damp(0.3) for b in channels.amplitude_damp(0.2)
+          for c in channels.amplitude_damp(0.25)]
+    P = [np.eye(2), gates.X(), gates.Y(), gates.Z()]
+    r = 0.05
+    dep3 = [np.sqrt(1 - r) * np.eye(8)] + [np.sqrt(r / 63) * np.kron(np.kron(P[i], P[j]), P[k])
+                                          for i in range(4) for j in range(4) for k in range(4) if (i, j, k) != (0, 0, 0)]
+    moms = []
+    for layer in range(3):
+        moms.append([Gate((q,), workloads.haar_unitary(rng, 2)) for q in range(n)])
+        moms.append([Gate((0, n - 1), workloads.haar_unitary(rng, 4)), Gate((2, 3), workloads.haar_unitary(rng, 4))])
+        moms.append([Channel((1, n - 2, 4), ad), Channel((0, 3, n - 1), dep3)])
+    c = Circuit(n_qubits=n, moments=moms, observables=["Z" * n, "X" + "I" * (n - 2) + "Z"])
+    ref, out, state = run_both(ctx, c, seed=23, T=16, shots=2, mode=mode)
+    assert (ref["branch"] == 1).any()
+    assert compare(ref, out, state) == 0
