@@ -239,6 +239,14 @@ qt_status qt_channel_first_loop(int nq, int n_kraus, const double* K, double u, 
                                 double* r_rest, double* deferred_scale);
 qt_status qt_channel_choose(int nq, int n_kraus, const double* K, const int* qubits, const double* rho,
                             double r, int mode, int* pick, double* scale);
+/* qt_readout_flips: readout error (R14) on recorded bitstrings of an
+ *   n-qubit register: bits[i] (bit q = qubit q) of shot shot_ids[i] of trajectory
+ *   traj; a recorded 0 becomes 1 when u < p00_err[q], a recorded 1 becomes 0 when
+ *   u < p11_err[q], u = the READOUT draw of (shot, q) (purpose 3, ordinal
+ *   shot * ceil(n/2) + q / 2, half q % 2), one draw per (shot, qubit) whatever the
+ *   bit.  p00_err / p11_err: n doubles or NULL.  In place; host only. */
+qt_status qt_readout_flips(int n, const double* p00_err, const double* p11_err, uint64_t seed, uint64_t traj,
+                           int nshots, const int32_t* shot_ids, uint64_t* bits);
 qt_status qt_apply_plan(qt_ctx ctx, qt_plan plan, void* state_dev, size_t state_bytes);
 qt_status qt_reduce_rho(qt_ctx ctx, const void* state_dev, int n, int nq, const int* qubits, double* out);
 qt_status qt_sample_local(qt_ctx ctx, const void* state_dev, int n, int n_total, uint64_t seed, uint64_t traj,

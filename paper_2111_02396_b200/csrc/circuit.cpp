@@ -230,6 +230,26 @@ qt_status qt_add_gate_sweep(qt_circuit c, int moment, int nq, const int* qubits,
 
 int qt_circuit_num_sets(qt_circuit c) { return c ? c->c.n_sets : 0; }
 
+qt_status qt_readout_flips(int n, const double* p00_err, const double* p11_err, uint64_t seed, uint64_t traj,
+                           int nshots, const int32_t* shot_ids, uint64_t* bits) {
+    if (n < 1 || n > 63 || nshots < 0 || (nshots > 0 && (!shot_ids || !bits)))
+        return fail(QT_EINVAL, "qt_readout_flips: bad arguments");
+    if (!p00_err && !p11_err) return QT_OK;
+    const uint32_t half_n = (uint32_t)(n + 1) / 2;
+    for (int i = 0; i < nshots; ++i) {
+        const uint64_t b = bits[i];
+        uint64_t o = b;
+        for (int q = 0; q < n; ++q) {
+            const double u = draw(seed, (uint32_t)shot_ids[i] * half_n + (uint32_t)(q / 2), kPurposeReadout, traj, q % 2);
+            const int bit = (int)((b >> q) & 1ull);
+            if (bit == 0 && p00_err && u < p00_err[q]) o |= 1ull << q;
+            if (bit == 1 && p11_err && u < p11_err[q]) o &= ~(1ull << q);
+        }
+        bits[i] = o;
+    }
+    return QT_OK;
+}
+
 double qt_draw(uint64_t seed, uint32_t ordinal, uint32_t purpose, uint64_t traj, int half) {
     return draw(seed, ordinal, purpose, traj, half);
 }

@@ -503,6 +503,10 @@ class DistributedTrajectory:
                     bits[sh] |= np.uint64(lb)
         for sh in range(shots):  # every rank ends with every shot's bits
             bits[sh:sh + 1] = self.f.broadcast_u64(bits[sh:sh + 1], int(owners[sh]))
+        out["bits_raw"] = bits.copy()
+        p00, p11 = getattr(circuit, "p00", None), getattr(circuit, "p11", None)
+        if shots > 0 and (p00 is not None or p11 is not None):  # readout error, same draws on every rank
+            bits = qtraj.readout_flips(bits, self.n, p00, p11, seed, traj)
         out["bits"] = bits
         out["masses"] = M
         return out

@@ -82,6 +82,8 @@ def lib() -> ctypes.CDLL:
         "qt_set_readout": ([vp, dp, dp], ctypes.c_int),
         "qt_circuit_num_recorded": ([vp], ctypes.c_int),
         "qt_add_gate_sweep": ([vp, ctypes.c_int, ctypes.c_int, ip, ctypes.c_int, dp], ctypes.c_int),
+        "qt_readout_flips": ([ctypes.c_int, dp, dp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ip,
+                              ctypes.POINTER(ctypes.c_uint64)], ctypes.c_int),
         "qt_circuit_num_sets": ([vp], ctypes.c_int),
         "qt_circuit_num_channels": ([vp], ctypes.c_int),
         "qt_fuse": ([vp, ctypes.c_int, ctypes.POINTER(vp)], ctypes.c_int),
@@ -374,6 +376,17 @@ PURPOSE_CHANNEL, PURPOSE_SAMPLE, PURPOSE_READOUT = 1, 2, 3
 def draw(seed: int, ordinal: int, purpose: int, traj: int, half: int = 0) -> float:
     """The RNG contract's uniform (Philox4x32-10, qtraj.h)."""
     return lib().qt_draw(seed, ordinal, purpose, traj, half)
+
+
+def readout_flips(bits: np.ndarray, n: int, p00, p11, seed: int, traj: int, shot_ids=None) -> np.ndarray:
+    """Readout error on recorded bitstrings (qt_readout_flips); returns a copy."""
+    out = np.ascontiguousarray(bits, dtype=np.uint64).copy()
+    ids = np.arange(len(out), dtype=np.int32) if shot_ids is None else np.ascontiguousarray(shot_ids, np.int32)
+    a = None if p00 is None else np.ascontiguousarray(p00, np.float64)
+    b = None if p11 is None else np.ascontiguousarray(p11, np.float64)
+    _check(lib().qt_readout_flips(n, None if a is None else _dptr(a), None if b is None else _dptr(b), seed, traj,
+                                  len(out), _iptr(ids), out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
+    return out
 
 
 def channel_first_loop(kraus, u: float, mode: int = 0):

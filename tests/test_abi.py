@@ -112,3 +112,16 @@ def test_fusion_reduces_passes_and_respects_f():
     assert seen[2] >= seen[3] >= seen[4]
     tiled = qtraj.Plan(circ, max_fused=4).info(workloads.trajectory_seed(2), 0)
     assert tiled["passes"] < seen[4]
+
+
+def test_readout_flips_match_oracle():
+    """qt_readout_flips (host, the distributed driver's readout) applied to the
+    oracle's raw samples gives the oracle's recorded samples (R14)."""
+    c = workloads.random_circuit(9, depth=4, seed=12, noise="depol", p=0.02, readout=True)
+    c.p00 = np.full(9, 0.2)
+    c.p11 = np.full(9, 0.3)
+    r = oracle.run_trajectories(c, seed=41, traj_count=20, shots=5)
+    assert (r["bits"] != r["bits_raw"]).any()
+    for t in range(20):
+        got = qtraj.readout_flips(r["bits_raw"][t], 9, c.p00, c.p11, 41, t)
+        assert np.array_equal(got, r["bits"][t])

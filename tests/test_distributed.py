@@ -96,7 +96,7 @@ class NumpyBackend:
 
 def circuit(n, seed, noise="both"):
     c = workloads.random_circuit(n, depth=6, seed=seed, max_arity=2, noise=noise, p=0.04,
-                                 t1_ns=600.0, tphi_ns=1000.0)
+                                 t1_ns=600.0, tphi_ns=1000.0, readout=True)
     c.observables = ["I" * q + "Z" + "I" * (n - q - 1) for q in range(n)] + ["Z" * n]
     return c
 
