@@ -372,6 +372,35 @@ class DistributedTrajectory:
             out[rk] = rho
         return out, pos
 
+    def _pauli_values(self, strings: Sequence[str]) -> np.ndarray:
+        """<P>/<psi|psi> of Pauli strings (char q = logical qubit q) whose X / Y
+        qubits are all local in the current layout."""
+        zvals = {}
+        for rk in self.f.local_ranks:
+            loc = []
+            for s_ in strings:
+                ls = ["I"] * self.nl
+                for q in range(self.n):
+                    if self.slot[q] < self.nl:
+                        ls[self.slot[q]] = s_[q]
+                    else:
+                        assert s_[q] in "IZ", "X / Y qubits must be local"
+                loc.append("".join(ls))
+            vals, norm = self.b.expect(self.states[rk], loc)
+            if not norm > 0.0:  # an empty slice (e.g. after amplitude damping): 0/0 partials
+                vals = np.zeros(len(loc))
+                norm = 0.0
+            sg = []
+            for s_ in strings:
+                par = 0
+                for q in range(self.n):
+                    if self.slot[q] >= self.nl and s_[q] == "Z":
+                        par ^= (rk >> (self.slot[q] - self.nl)) & 1
+                sg.append(-1.0 if par else 1.0)
+            zvals[rk] = np.asarray([sgn * v * norm for sgn, v in zip(sg, vals)] + [norm], np.float64)
+        tot = self.f.allreduce(zvals)
+        return tot[:-1] / tot[-1]
+
     def _ensure_local(self, qubits: Sequence[int], upcoming: List[set]):
         """Make `qubits` local.  The all-to-all of an s-qubit swap moves (1 - 2^-s) of
         the state, so other global qubits ride along when they are used (within the
@@ -440,6 +469,25 @@ class DistributedTrajectory:
             kraus_rec.append(pick)
             ch += 1
         self._flush()
+        out = {"kraus": np.array(kraus_rec, np.int32)}
+        # Pauli expectations: a string's X / Y qubits must be local (the operator is
+        # then block-diagonal over the ranks; its global Z bits give a sign per
+        # rank).  Strings that need no swap are evaluated together; the others
+        # swap their X / Y qubits in first (one string at a time).
+        if observables:
+            vals = np.zeros(len(observables))
+            ready = [i for i, s_ in enumerate(observables)
+                     if all(self.slot[q] < self.nl for q in range(self.n) if s_[q] in "XY")]
+            later = [i for i in range(len(observables)) if i not in ready]
+            if ready:
+                vals[ready] = self._pauli_values([observables[i] for i in ready])
+            for i in later:
+                xy = [q for q in range(self.n) if observables[i][q] in "XY"]
+                if len(xy) > self.nl:
+                    raise ValueError(f"distributed mode: a Pauli string needs at most {self.nl} X / Y qubits")
+                self._ensure_local(xy, [])
+                vals[i] = self._pauli_values([observables[i]])[0]
+            out["obs"] = vals
         # layout for sampling: logical qubits >= nl global, local slot i = logical i
         high_local = [q for q in range(self.nl, self.n) if self.slot[q] < self.nl]
         low_global = [q for q in range(self.nl) if self.slot[q] >= self.nl]
@@ -447,32 +495,13 @@ class DistributedTrajectory:
             self._swap_in(low_global, high_local)
         self._apply_local_perm({self.slot[q]: q for q in range(self.nl) if self.slot[q] != q})
         assert all(self.slot[q] == q for q in range(self.nl))
-        out = {"kraus": np.array(kraus_rec, np.int32), "swaps": self.swaps}
-        # rank masses and observables
+        out["swaps"] = self.swaps
+        # rank masses for the chain rule over the rank bits
         masses = {}
-        zvals = {}
         for rk in self.f.local_ranks:
-            obs_local = []
-            for s_ in observables:
-                assert all(ch_ in "IZ" for ch_ in s_), "distributed mode: Z-type observables"
-                obs_local.append("".join(s_[q] for q in range(self.nl)))
-            vals, norm = self.b.expect(self.states[rk], obs_local)
-            if not norm > 0.0:  # an empty slice (e.g. after amplitude damping): 0/0 partials
-                vals = np.zeros(len(obs_local))
-                norm = 0.0
-            masses[rk] = norm
-            sg = []
-            for s_ in observables:
-                par = 0
-                for q in range(self.nl, self.n):
-                    if s_[q] == "Z":
-                        par ^= (rk >> (self.slot[q] - self.nl)) & 1
-                sg.append(-1.0 if par else 1.0)
-            zvals[rk] = np.asarray([sgn * v * norm for sgn, v in zip(sg, vals)] + [norm], np.float64)
+            _, norm = self.b.expect(self.states[rk], [])
+            masses[rk] = norm if norm > 0.0 else 0.0
         M = self.f.allgather(masses)
-        if observables:
-            tot = self.f.allreduce(zvals)
-            out["obs"] = tot[:-1] / tot[-1]
         # chain rule over the rank bits (levels n-1 .. nl), then local levels on the owner
         half_n = (self.n + 1) // 2
         bits = np.zeros(shots, np.uint64)

@@ -63,15 +63,10 @@ class NumpyBackend:
 
     def expect(self, state, observables):
         psi = state.numpy()
-        p = np.abs(psi) ** 2
-        norm = float(p.sum())
-        idx = np.arange(psi.size)
-        vals = []
-        for s in observables:
-            z = sum(1 << q for q, ch in enumerate(s) if ch == "Z")
-            par = np.array([bin(int(i) & z).count("1") & 1 for i in idx])
-            vals.append(float(np.sum(np.where(par, -p, p)) / norm))
-        return np.array(vals), norm
+        norm = float(np.sum(np.abs(psi) ** 2))
+        if not norm > 0.0:
+            return np.zeros(len(observables)), 0.0
+        return np.array([oracle.pauli_expectation(psi, s) for s in observables]), norm
 
     def sample_local(self, state, n_total, seed, traj, shot_ids):
         psi = state.numpy()
@@ -128,6 +123,23 @@ def test_emulated_fabric_numpy_backend_matches_oracle(world):
         out = tr.run(c, seed=seed, traj=t, shots=2, observables=c.observables)
         check(out, ref, t)
         assert out["swaps"] > 0
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_xy_observables_on_global_qubits(world):
+    """Pauli strings with X / Y on global (rank-index) qubits: their qubits are
+    swapped in before the evaluation (block-diagonal over ranks); values equal the
+    oracle's, and the sampler still sees the logical layout."""
+    n = 9
+    c = circuit(n, seed=8)
+    c.observables = ["I" * (n - 1) + "X", "Y" + "I" * (n - 2) + "X", "I" * (n - 3) + "YZX", "XZXZXZXIY",
+                     "Z" + "I" * (n - 2) + "Y", "I" * n]
+    seed, T = 5, 3
+    ref = oracle.run_trajectories(c, seed=seed, traj_count=T, shots=3)
+    for t in range(T):
+        tr = D.DistributedTrajectory(NumpyBackend(), D.EmulatedFabric(world), n)
+        out = tr.run(c, seed=seed, traj=t, shots=3, observables=c.observables)
+        check(out, ref, t)
 
 
 def _free_port():
@@ -191,6 +203,7 @@ def test_gpu_backend_emulated_fabric_matches_oracle(world):
     ctx = qtraj.Context(0)
     n = 13
     c = circuit(n, seed=40 + world, noise="ad")
+    c.observables += ["I" * (n - 1) + "X", "Y" + "I" * (n - 3) + "ZX", "XZ" + "I" * (n - 4) + "YY"]
     seed, T = 99, 3
     ref = oracle.run_trajectories(c, seed=seed, traj_count=T, shots=3)
     for t in range(T):
