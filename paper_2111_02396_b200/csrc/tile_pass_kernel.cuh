@@ -19,6 +19,10 @@
 
 #include "tile_pass.cuh"
 
+#ifndef QT_TC4_MINB
+#define QT_TC4_MINB 4  // CTAs per SM of the 4-qubit tensor-core K1 (launch bounds)
+#endif
+
 namespace qt {
 
 namespace detail {
@@ -583,7 +587,7 @@ struct TileCfg {
 
 template <int T, int R, bool TC, int TCK = 4>
 __global__ void __launch_bounds__(TileCfg<T, R, TC, TCK>::NT,
-                                  TC ? (TCK == 6 ? 2 : (TCK == 5 ? 3 : 4)) : ((R <= 4 && T == 12) ? QT_MINB : 1))
+                                  TC ? (TCK == 6 ? 2 : (TCK == 5 ? 3 : QT_TC4_MINB)) : ((R <= 4 && T == 12) ? QT_MINB : 1))
 tile_pass_kernel(const TileArgs A, const int step) {
     using Cfg = TileCfg<T, R, TC, TCK>;
     // TMEM: TCK = 4: f16 runs use D of both groups (2 x 64 columns), 3xTF32 single
