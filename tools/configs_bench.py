@@ -1,5 +1,8 @@
 """Measured runs of the SURVEY 8(d) configs other than the bench line (C2):
 
+  C1     GHZ-4 with depolarizing 0.01 after every gate, 1 000 trajectories in one
+         batch (launch-latency bound: the whole state is one 128-byte tile).
+
   C3     26-qubit low-noise grid (2 x 13, 20 cycles, depolarize 1e-3 after every
          gate + phase_damp 1e-4 on every qubit per moment), f = 4, 5, 6: trajectories/s,
          passes and fused gates per trajectory, deferral fraction, reductions.
@@ -56,6 +59,8 @@ def main():
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6553.0) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6553.0
     ctx = qtraj.Context(0)
+    c1 = workloads.ghz4_depolarized(0.01)
+    run(ctx, c1, "C1 GHZ-4 depolarizing 0.01", 4, 1000, 1000, workloads.trajectory_seed(1), peak)
     c3 = workloads.low_noise_grid(config=3)
     for f in (4, 5, 6):
         run(ctx, c3, "C3 26q low-noise grid", f, a.c3_traj, 32, workloads.trajectory_seed(3), peak)
