@@ -29,7 +29,7 @@ def main():
     a = ap.parse_args()
     ctx = qtraj.Context(0)
     for n in [int(x) for x in a.qubits.split(",")]:
-        rows, cols = (4, 5) if n == 20 else (2, n // 2)
+        rows, cols = {20: (4, 5), 27: (3, 9)}.get(n, (2, n // 2))
         for g in [float(x) for x in a.gammas.split(",")]:
             # pure phase damping (depol = 0 drops the depolarizing channels), as in Fig. perf_noise
             c = workloads.low_noise_grid(rows=rows, cols=cols, cycles=a.cycles, config=3, depol=0.0, gamma_pd=g)
