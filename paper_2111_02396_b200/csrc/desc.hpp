@@ -49,7 +49,8 @@ struct GateDesc {
     uint32_t rpos;
     uint32_t tpos;
     uint16_t xu[12];      // TC runs: next-gate operand offsets of this gate's roles
-    uint32_t pad[2];
+    int32_t pair;         // TC runs: outputs c, c ^ 1 share a 16-byte chunk of the next operand
+    uint32_t pad;
 };
 static_assert(sizeof(GateDesc) == 48, "GateDesc layout");
 

@@ -343,6 +343,44 @@ int rank4(const unsigned* v, int count) {
 void tc_relayout(GateDesc& gd, const GateDesc* nx, int T, int grp, bool run_start = false) {
     uint32_t cfg = 0;
     for (int m = 0; m < 4; ++m) cfg |= 1u << ((gd.rpos >> (4 * m)) & 15u);
+    if (gd.pair) {
+        // paired 16-byte stores: a quarter-warp's 8 lanes must hit 8 distinct chunks
+        // (address bits 4..6: bank vectors without bit 0); among those choices the
+        // run-start fp32 gather (4 lanes, 2^(b mod 4)) decides
+        int cand[12], nc = 0;
+        for (int b = 0; b < T; ++b)
+            if (!(((cfg | (1u << grp)) >> b) & 1u)) cand[nc++] = b;
+        int best[4] = {-1, -1, -1, -1}, best_score = -1;
+        for (int a = 0; a < nc; ++a)
+            for (int b = 0; b < nc; ++b)
+                for (int c = 0; c < nc; ++c)
+                    for (int d = 0; d < nc; ++d) {
+                        if (b <= a || c <= b || a == d || b == d || c == d) continue;  // lanes 0-2 ascending, lane 3 any
+                        const int pick[4] = {cand[a], cand[b], cand[c], cand[d]};
+                        unsigned vs[3], vg[4];
+                        for (int i = 0; i < 3; ++i) vs[i] = bank_vec(nx, pick[i]) >> 1;
+                        for (int i = 0; i < 4; ++i) vg[i] = 1u << (pick[i] & 3);
+                        const int score = 8 * rank4(vs, 3) + (run_start ? rank4(vg, 4) : 0);
+                        if (score > best_score) {
+                            best_score = score;
+                            for (int i = 0; i < 4; ++i) best[i] = pick[i];
+                        }
+                    }
+        if (best_score >= 0) {
+            int lanes[12], nl = 0;
+            uint32_t used = cfg | (1u << grp);
+            for (int i = 0; i < 4; ++i) {
+                lanes[nl++] = best[i];
+                used |= 1u << best[i];
+            }
+            for (int b = 0; b < T; ++b)
+                if (!((used >> b) & 1u)) lanes[nl++] = b;
+            gd.rpos = (gd.rpos & 0xffffu) | ((uint32_t)grp << 16);
+            gd.tpos = 0;
+            for (int i = 0; i < nl; ++i) gd.tpos |= (uint32_t)lanes[i] << (4 * i);
+            return;
+        }
+    }
     if (run_start) {
         int cand[12], nc = 0;
         for (int b = 0; b < T; ++b)
@@ -410,7 +448,8 @@ void tc_relayout(GateDesc& gd, const GateDesc* nx, int T, int grp, bool run_star
 // contractions, widened by 2^shift); layouts are chosen last gate first for
 // conflict-free stores into the next layout; xu = next-gate operand offsets
 // of this gate's roles when the run continues.
-void tc_runs(GateDesc* gd, const double* norms, int count, int T) {
+void tc_runs(GateDesc* gd, const double* norms, int count, int T, std::vector<FusedDesc>& fused,
+             std::vector<ConsDesc>& cons, const int* gate_fused) {
     auto cfg_of = [&](int g) {
         uint32_t c = 0;
         for (int m = 0; m < 4; ++m) c |= 1u << ((gd[g].rpos >> (4 * m)) & 15u);
@@ -456,9 +495,37 @@ void tc_runs(GateDesc* gd, const double* norms, int count, int T) {
         for (int x = g; x <= e; ++x) grp[x] = b;
         g = e + 1;
     }
-    for (int g = count - 1; g >= 0; --g)
-        if (gd[g].k & kGateF16)
-            tc_relayout(gd[g], chained(g) ? &gd[g + 1] : nullptr, T, grp[g], !(g > 0 && chained(g - 1)));
+    for (int g = count - 1; g >= 0; --g) {
+        if (!(gd[g].k & kGateF16)) continue;
+        gd[g].pair = 0;
+        if (chained(g) && gate_fused[g] >= 0) {
+            // the next gate's matrix bit 0 is address bit 3 (the 8-byte half of a
+            // chunk): if it is one of this gate's matrix bits m0, relabel this gate's
+            // matrix bits 0 <-> m0 (register order and its constituents' positions,
+            // so K6 builds W in that order); outputs c, c ^ 1 then share a chunk
+            const uint32_t t0 = gd[g + 1].rpos & 15u;
+            int m0 = -1;
+            for (int m = 0; m < 4; ++m)
+                if (((gd[g].rpos >> (4 * m)) & 15u) == t0) m0 = m;
+            if (m0 > 0) {
+                const uint32_t r0 = gd[g].rpos & 15u, rm = (gd[g].rpos >> (4 * m0)) & 15u;
+                gd[g].rpos = (gd[g].rpos & ~(15u | (15u << (4 * m0)))) | rm | (r0 << (4 * m0));
+                const FusedDesc& fd = fused[gate_fused[g]];
+                for (int ci = fd.cons_begin; ci < fd.cons_begin + fd.cons_count; ++ci) {
+                    uint32_t pos = cons[ci].pos;
+                    // K6 reads the first nq (<= 6) nibbles; the others are ignored
+                    for (int j = 0; j < 6; ++j) {
+                        const uint32_t p = (pos >> (4 * j)) & 15u;
+                        const uint32_t q = p == 0u ? (uint32_t)m0 : (p == (uint32_t)m0 ? 0u : p);
+                        pos = (pos & ~(15u << (4 * j))) | (q << (4 * j));
+                    }
+                    cons[ci].pos = pos;
+                }
+            }
+            if (m0 >= 0) gd[g].pair = 1;
+        }
+        tc_relayout(gd[g], chained(g) ? &gd[g + 1] : nullptr, T, grp[g], !(g > 0 && chained(g - 1)));
+    }
     for (int g = 0; g < count; ++g) {
         if (!chained(g)) continue;
         for (int r = 0; r < 12; ++r) {
@@ -674,7 +741,8 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
                 gate_layout(gate_masks[pd.gate_begin + g], pd.tile_mask, T, R, gd.rpos, gd.tpos);
             }
             if (P.tc && P.tc_k == 4) {
-                tc_runs(out.gates.data() + pd.gate_begin, gate_norms.data() + pd.gate_begin, pd.gate_count, T);
+                tc_runs(out.gates.data() + pd.gate_begin, gate_norms.data() + pd.gate_begin, pd.gate_count, T,
+                        out.fused, out.cons, gate_fused.data() + pd.gate_begin);
                 for (int g = 0; g < pd.gate_count; ++g)
                     if (out.gates[pd.gate_begin + g].k & kGateF16) out.fused[gate_fused[pd.gate_begin + g]].k |= kGateF16;
             }

@@ -1058,6 +1058,7 @@ extern "C" qt_status qt_plan_bank_stats(qt_plan plan, uint64_t seed, uint64_t tr
                             out[3] += halfwarp_wavefronts(a);
                         }
                         if (chained) {
+                            if (G.pair && (c & 1)) continue;  // stored with c - 1 (16-byte store)
                             for (int l = 0; l < 32; ++l) {
                                 const uint32_t tid = (uint32_t)(warp * 32 + l);
                                 uint32_t o = 0;
@@ -1068,7 +1069,15 @@ extern "C" qt_status qt_plan_bank_stats(qt_plan plan, uint64_t seed, uint64_t tr
                                 a[l] = o;
                             }
                             out[0] += 1;
-                            out[1] += halfwarp_wavefronts(a);
+                            if (G.pair) {  // quarter-warps of 8 lanes x 16 bytes, 8 chunks per 128 bytes
+                                for (int qw = 0; qw < 4; ++qw) {
+                                    int cnt[8] = {0}, mx = 0;
+                                    for (int l = 0; l < 8; ++l) mx = std::max(mx, ++cnt[(a[8 * qw + l] >> 4) & 7u]);
+                                    out[1] += mx;
+                                }
+                            } else {
+                                out[1] += halfwarp_wavefronts(a);
+                            }
                         } else {
                             fp32_addrs(G, warp, g, c, a);
                             out[4] += 1;

@@ -186,11 +186,23 @@ __device__ __forceinline__ int tc_run_f16(float2* tile, unsigned char* mbuf, uin
     __syncwarp();
     const uint32_t lane_off = (warp * 32u) << 16;
     // read D[grp] of this thread's row, write the 16 outputs (split or fp32)
-    auto readout = [&](int grp, uint32_t b, const uint32_t (&lo)[16], bool chain, uint64_t inv2) {
+    auto readout = [&](int grp, uint32_t b, const uint32_t (&lo)[16], bool chain, uint64_t inv2, bool pair) {
         uint32_t h0[32], h1[32];
         tmem_ld32(tmem + lane_off + 64 * grp, h0);
         tmem_ld32(tmem + lane_off + 64 * grp + 32, h1);
         tmem_wait_ld();
+        if (pair) {  // outputs c, c ^ 1 fill one 16-byte chunk (lo[c ^ 1] = lo[c] ^ 8)
+#pragma unroll
+            for (int c = 0; c < 16; c += 2) {
+                const uint2 x0 = split_f16(add2(pk2(__uint_as_float(h0[2 * c]), __uint_as_float(h0[2 * c + 1])),
+                                                pk2(__uint_as_float(h1[2 * c]), __uint_as_float(h1[2 * c + 1]))));
+                const uint2 x1 =
+                    split_f16(add2(pk2(__uint_as_float(h0[2 * c + 2]), __uint_as_float(h0[2 * c + 3])),
+                                   pk2(__uint_as_float(h1[2 * c + 2]), __uint_as_float(h1[2 * c + 3]))));
+                *reinterpret_cast<uint4*>(tb8 + (b ^ lo[c])) = make_uint4(x0.x, x0.y, x1.x, x1.y);
+            }
+            return;
+        }
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
             const uint64_t y = add2(pk2(__uint_as_float(h0[2 * c]), __uint_as_float(h0[2 * c + 1])),
@@ -229,8 +241,8 @@ __device__ __forceinline__ int tc_run_f16(float2* tile, unsigned char* mbuf, uin
             mbar_wait(mbar + 1, ph[1]);
             ph[1] ^= 1u;
             fence_after();
-            readout(0, obase, lo, true, 0);
-            readout(1, obase ^ xu[4], lo, true, 0);
+            readout(0, obase, lo, true, 0, G.pair != 0);
+            readout(1, obase ^ xu[4], lo, true, 0, G.pair != 0);
             if (g + 2 < ng) {  // both MMAs of gate g are done: its W buffer takes W(g + 2)
                 const char* src = reinterpret_cast<const char*>(pool + gdesc[g + 2].mat_off);
                 unsigned char* dst = mbuf + (g & 1) * mbuf_bytes;
@@ -260,7 +272,7 @@ __device__ __forceinline__ int tc_run_f16(float2* tile, unsigned char* mbuf, uin
         ph[0] ^= 1u;
         fence_after();
         QT_MARK(1);
-        readout(0, obase, lo, true, 0);
+        readout(0, obase, lo, true, 0, G.pair != 0);
         QT_MARK(2);
         cp_async_wait_all();  // W(g + 1)
         fence_proxy_async();
@@ -274,7 +286,7 @@ __device__ __forceinline__ int tc_run_f16(float2* tile, unsigned char* mbuf, uin
         ph[1] ^= 1u;
         fence_after();
         QT_MARK(4);
-        readout(1, obase ^ xu[4], lo, true, 0);
+        readout(1, obase ^ xu[4], lo, true, 0, G.pair != 0);
         QT_MARK(5);
         if (g + 2 < ng) {  // both MMAs of gate g are done: its W buffer takes W(g + 2)
             const char* src = reinterpret_cast<const char*>(pool + gdesc[g + 2].mat_off);
@@ -308,7 +320,7 @@ __device__ __forceinline__ int tc_run_f16(float2* tile, unsigned char* mbuf, uin
         fence_after();
         const uint64_t inv2 = pk2(run_inv, run_inv);
 #pragma unroll 1
-        for (int grp = 0; grp < 2; ++grp) readout(grp, obase ^ (grp ? ogrp : 0u), lo, false, inv2);
+        for (int grp = 0; grp < 2; ++grp) readout(grp, obase ^ (grp ? ogrp : 0u), lo, false, inv2, false);
         fence_before();
     }
     return g1;
