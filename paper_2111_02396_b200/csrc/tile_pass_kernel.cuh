@@ -10,10 +10,13 @@
 //               tile in the f16 operand layout: each gate's epilogue reads D
 //               from TMEM and writes it straight into the next gate's operand
 //               layout (one barrier and one MMA round trip per gate, no
-//               gather).  Gates flagged non-TC (the device-chosen operators of
-//               conventional channels, k <= 2) use the CUDA-core path with
-//               R = 5 on the fp32 tile.  TCK = 5 (f = 5 plans): 3xTF32 with A
-//               in TMEM, one gate at a time.
+//               gather; outputs c, c ^ 1 go out as one 16-byte store when the
+//               planner has relabelled the gate's matrix bits, GateDesc::pair).
+//               Gates flagged non-TC (the device-chosen operators of
+//               conventional channels, k <= 3) use the CUDA-core path with
+//               R = 5 on the fp32 tile.  Single 4-qubit gates: 3xTF32 with A in
+//               TMEM.  TCK = 5 / 6 (f = 5 / 6 plans): f16 hi/lo GEMMs, one wide
+//               gate at a time (apply_tc_wide).
 #pragma once
 #include <cuda_fp16.h>
 
