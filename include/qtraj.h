@@ -137,7 +137,9 @@ qt_status qt_fuse(qt_circuit c, int max_fused, qt_plan* out);
 
 typedef struct {
     int max_fused;    /* f in [2, 6]; 0 = 4 */
-    int tile_bits;    /* qubits held per CTA tile; 0 = auto (12, or n if n < 12) */
+    int tile_bits;    /* qubits held per tile; 0 = auto: 13 for n >= 13 with 4-qubit tensor-core
+                         gates (persistent TMEM kernel), else 12, or n if n < 12; 12 forces the
+                         per-tile kernel */
     int low_bits;     /* lowest qubits always in a tile (coalescing); 0 = auto (4) */
     int one_gate_per_pass; /* 1 = every fused gate is its own HBM pass (the paper's GPU scheme) */
     int tensor_cores;      /* 0 = auto (on when n >= 12; fused gates padded to max(f, 4) qubits),

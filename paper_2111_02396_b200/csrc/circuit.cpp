@@ -3,6 +3,7 @@
 // mixtures P:186).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -427,20 +428,31 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
     Plan& P = hp->p;
     const Circuit& C = c->c;
     P.n = C.n;
-    P.T = o.tile_bits ? o.tile_bits : std::min(C.n, 12);
-    if (P.T > 12 || P.T > C.n || P.T < 1) {
-        delete hp;
-        return fail(QT_EINVAL, "tile_bits must be <= min(n, 12)");
-    }
-    if (C.n > 12 && P.T != 12) {
-        delete hp;
-        return fail(QT_EINVAL, "tile_bits must be 12 for n > 12 in this build");
-    }
-    P.CL = std::min(o.low_bits ? o.low_bits : 4, P.T);
     // register width: 2^R amplitudes per thread; must hold every fused gate
     int max_arity = 1;
     for (auto& op : C.ops) max_arity = std::max(max_arity, op.nq);
-    if (P.T == 12) {
+    // the persistent TMEM kernel (4-qubit tensor-core gates on 13-qubit tiles) is the
+    // default for n >= 13 (tile_bits 0 or 13); tile_bits = 12 selects the per-tile kernel
+    const bool v2_ok = C.n >= 13 && o.tensor_cores >= 0 && f <= 4 && max_arity <= f &&
+                       (o.tile_bits == 0 || o.tile_bits == 13) && o.low_bits == 0;
+    // (default while the persistent kernel is being tuned: opt in with QT_TILE13=1 or tile_bits = 13)
+    const char* env13 = std::getenv("QT_TILE13");
+    const bool auto13 = env13 && env13[0] == '1';
+    P.T = o.tile_bits ? o.tile_bits : std::min(C.n, (v2_ok && auto13) ? 13 : 12);
+    if (P.T == 13 && !v2_ok) {
+        delete hp;
+        return fail(QT_EINVAL, "tile_bits = 13 needs n >= 13, tensor cores and max_fused <= 4");
+    }
+    if ((P.T > 12 && P.T != 13) || P.T > C.n || P.T < 1) {
+        delete hp;
+        return fail(QT_EINVAL, "tile_bits must be <= min(n, 12), or 13");
+    }
+    if (C.n > 12 && P.T != 12 && P.T != 13) {
+        delete hp;
+        return fail(QT_EINVAL, "tile_bits must be 12 or 13 for n > 12 in this build");
+    }
+    P.CL = std::min(o.low_bits ? o.low_bits : 4, P.T);
+    if (P.T >= 12) {
         P.R = std::max(f <= 4 ? 4 : f, max_arity);
     } else {
         // whole-state tiles (n < 12): 2^R amplitudes per thread hold the widest gate
@@ -450,7 +462,7 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
     P.one_gate = o.one_gate_per_pass != 0;
     // tensor cores: every fused gate padded to 4 qubits (f <= 4), T = 12, 128-thread CTAs
     // whose CUDA-core gates use R = 5
-    const bool tc_ok = (P.T == 12 && max_arity <= f);
+    const bool tc_ok = ((P.T == 12 || P.T == 13) && max_arity <= f);
     if (o.tensor_cores > 0 && !tc_ok) {
         delete hp;
         return fail(QT_EINVAL, "tensor_cores needs n >= 12 and gates of <= max_fused qubits");
@@ -464,6 +476,12 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
         P.R = 5;
         P.f = f;
         P.tc_k = f <= 4 ? 4 : f;
+        // T = 13: 128 threads per compute warpgroup hold 64 amplitudes each for the
+        // CUDA-core gates (device-chosen conventional operators)
+        if (P.T == 13) {
+            P.v2 = true;
+            P.R = 6;
+        }
     }
     // canonical order: moment ascending, then call order (stable)
     std::vector<const HostOp*> order;
@@ -603,6 +621,8 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
                     return fail(QT_EINVAL, "tensor_cores: a matrix of norm > 1e3 does not fit the f16 operands");
                 }
                 P.tc = false;
+                P.v2 = false;
+                if (P.T == 13) P.T = 12;  // the CUDA-core kernel tiles 12 qubits
                 P.R = std::max(f <= 4 ? 4 : f, max_arity);
                 P.f = std::min(f, P.R);
                 break;

@@ -25,9 +25,11 @@ struct PassDesc {
     int32_t event;        // EventDesc index (kPassRho) or -1
     int32_t obs_begin;    // into ObsDesc[] (kPassObs)
     int32_t obs_count;
-    uint8_t tq[12];       // global qubit of tile bit i (ascending), i < T
+    uint8_t tq[16];       // global qubit of tile bit i (ascending), i < T
     int32_t slot;         // batch slot (set by the executor in the per-step launch arrays)
+    int32_t pad;
 };
+static_assert(sizeof(PassDesc) == 56, "PassDesc layout");
 
 // A fused gate inside a pass and the register layout used to apply it:
 // register bit m of a thread's 2^R amplitudes <-> tile-local bit rpos[m]
@@ -63,6 +65,16 @@ constexpr int32_t kGateTC = 0x100;
 constexpr int32_t kGateRunStart = 0x200;  // first gate of a tensor-core run
 constexpr int32_t kGateF16 = 0x400;       // 4-qubit gate of a run of >= 2: f16 operands (else 3xTF32)
 constexpr int kGateShiftBit = 16;         // bits 16..23: run scale headroom (log2)
+// Persistent TMEM kernel (tile_pass_v2.cu, T = 13 tiles, 4-qubit gates):
+//   rpos nibbles 0..3 = tile bits of matrix bits 0..3 (config), 4..5 = group bits;
+//   tpos nibbles 0..6 = tile bits of TMEM lane bits 0..4 and warp bits 0..1;
+//   kGateRunStart: gather the fp32 tile into TMEM operand A (new f16 tile scale);
+//   kGateRunEnd: write D back to the fp32 tile; otherwise xu[0..5] = TMEM column
+//   offset, in this gate's D, of the next gate's config bits 0..3 / group bits 0..1.
+constexpr int32_t kGateV2 = 0x800;
+constexpr int32_t kGateRunEnd = 0x1000;
+// Pool bytes of a v2 gate operand: B = 32 rows x [W_hi (32 f16) | W_lo (32 f16)], SWIZZLE_128B.
+constexpr int kV2GateBytes = 4096;
 // Pool bytes of a tensor-core gate operand padded to k qubits (tc_common.cuh
 // gate_bytes): 4 -> f16 B or tf32 hi/lo W (8 KB), 5 -> f16 hi/lo B (16 KB),
 // 6 -> f16 hi/lo B in two K-chunks of 256 rows (64 KB).

@@ -68,6 +68,7 @@ struct Plan {
     bool one_gate = false;
     bool tc = false;    // fused gates padded to tc_k qubits and applied on tcgen05 tensor cores
     int tc_k = 4;       // 4 (f <= 4), 5 (f = 5) or 6 (f = 6)
+    bool v2 = false;    // tc_k == 4 on n >= 13 qubits: T = 13 tiles, persistent TMEM kernel (tile_pass_v2.cu)
     std::vector<PlanOp> ops;
     std::vector<Variant> vars;
     std::vector<VarDesc> var_desc;

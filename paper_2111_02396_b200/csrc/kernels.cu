@@ -38,6 +38,7 @@ cudaError_t launch_tile_pass_r6s_a(const TileArgs& a, int step, uint32_t ntiles,
 cudaError_t launch_tile_pass_r6s_b(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s);
 cudaError_t launch_tile_pass_r6(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s);
 cudaError_t launch_tile_pass_tc(const TileArgs& a, int tck, int step, uint32_t ntiles, int nslots, cudaStream_t s);
+cudaError_t launch_tile_pass_v2(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s);
 
 size_t tile_pass_smem_bytes(int T, int R, int tck) { return tile_pass_smem_bytes_impl(T, R, tck != 0, tck ? tck : 4); }
 
@@ -47,6 +48,7 @@ cudaError_t launch_tile_pass(const TileArgs& a, int R, int tck, int step, uint32
     // T = 1..11 (the whole state of n < 12 qubits in one CTA) and (T, 5 | 6) for
     // T = R..11 (5- and 6-qubit gates on small registers); tensor cores
     // (tck = 4, 5 or 6 qubits per padded gate): (12, 5).
+    if (a.T == 13) return tck == 4 ? launch_tile_pass_v2(a, step, ntiles, nslots, s) : cudaErrorInvalidValue;
     if (tck) return a.T == 12 && R == 5 ? launch_tile_pass_tc(a, tck, step, ntiles, nslots, s) : cudaErrorInvalidValue;
     if (a.T == 12 && R == 6) return launch_tile_pass_r6(a, step, ntiles, nslots, s);
     if (a.T == 12 && R == 5) return launch_tile_pass_r5(a, step, ntiles, nslots, s);
@@ -118,6 +120,26 @@ materialize_kernel(const FusedDesc* __restrict__ fused, const ConsDesc* __restri
     if (!tcm) {
         for (int e = threadIdx.x; e < DD; e += kMatThreads)
             pool[F.mat_off + e] = make_float2((float)v[e].x, (float)v[e].y);
+        return;
+    }
+    if (F.k & kGateV2) {
+        // persistent TMEM kernel operand (desc.hpp kV2GateBytes): B row n = 2j + b holds
+        // W[n][2c + a] = blk[a][b] of U[j][c] as f16 hi (bytes 0..63) and lo (64..127),
+        // SWIZZLE_128B K-major, 32 rows
+        __half* B = reinterpret_cast<__half*>(pool + F.mat_off);
+        for (int e = threadIdx.x; e < DD; e += kMatThreads) {
+            const int jj = e / D, c = e % D;
+            const double ur = v[e].x, ui = v[e].y;
+            const double blk[2][2] = {{ur, ui}, {-ui, ur}};
+            for (int a2 = 0; a2 < 2; ++a2)
+                for (int b = 0; b < 2; ++b) {
+                    const double w = blk[a2][b];
+                    const __half h = __double2half(w);
+                    const __half l = __double2half(w - (double)__half2float(h));
+                    B[tc::sw128_offset(2 * jj + b, 2 * (2 * c + a2)) >> 1] = h;
+                    B[tc::sw128_offset(2 * jj + b, 64 + 2 * (2 * c + a2)) >> 1] = l;
+                }
+        }
         return;
     }
     if (k == 4 && (F.k & kGateF16)) {

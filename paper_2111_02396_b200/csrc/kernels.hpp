@@ -38,7 +38,7 @@ struct TileArgs {
 
 // Largest register width R (amplitudes per thread = 2^R) compiled.
 constexpr int kMaxR = 6;
-constexpr int kMaxT = 12;
+constexpr int kMaxT = 13;
 
 size_t tile_pass_smem_bytes(int T, int R, int tck);
 // tck: 0 = CUDA-core fused gates; 4 / 5 / 6 = tensor-core gates padded to tck qubits.

@@ -535,6 +535,98 @@ void tc_runs(GateDesc* gd, const double* norms, int count, int T, std::vector<Fu
     }
 }
 
+// Persistent TMEM kernel layouts (tile_pass_v2.cu, T = 13).  A fused 4-qubit gate
+// is one M128 x N32 x K96 real GEMM per group: 7 tile bits index the 128 TMEM lanes
+// (rows), 2 are group bits (four D / A column blocks per thread) and its 4 matrix
+// bits are the columns.  Consecutive gates whose qubits, together, fit in 6 tile
+// bits form a SEGMENT with one row set: between them the epilogue reads D and
+// writes the next A inside TMEM (each thread keeps its row; only the roles of the
+// 6 thread-local bits change), with the next gate's source columns xu.  A segment
+// starts by gathering the fp32 tile from shared memory and ends by writing it back.
+namespace {
+inline unsigned v2_bank(int b) {  // slot bits 0..3 of tile bit b under the T = 13 swizzle
+    if (b == 0) return 1u;
+    if (b < 4) return 1u << b;
+    return 2u << ((b - 4) % 3);
+}
+}  // namespace
+
+void v2_layouts(GateDesc* gd, const uint32_t* lmask, const double* norms, int count) {
+    constexpr int T = 13;
+    for (int g = 0; g < count;) {
+        if (!(gd[g].k & kGateTC)) {
+            ++g;
+            continue;
+        }
+        // segment [g, e]: union of the gates' tile bits <= 6, norm product <= 16
+        uint32_t local = lmask[g];
+        double cum = norms[g];
+        int e = g;
+        while (e + 1 < count && (gd[e + 1].k & kGateTC) && __builtin_popcount(local | lmask[e + 1]) <= 6 &&
+               cum * norms[e + 1] <= 16.0) {
+            ++e;
+            local |= lmask[e];
+            cum *= norms[e];
+        }
+        // pad the thread-local set to 6 bits with the highest free tile bits (the low
+        // ones stay lane bits: bank-conflict-free gathers)
+        for (int b = T - 1; b >= 0 && __builtin_popcount(local) < 6; --b) local |= 1u << b;
+        // lane bits 0..3: GF(2)-independent bank vectors first (tile bit 0 first)
+        int rows[7], nr = 0;
+        unsigned basis[4] = {0, 0, 0, 0};
+        uint32_t used = local;
+        for (int pass = 0; pass < 2; ++pass)
+            for (int b = 0; b < T && nr < 4; ++b) {
+                if ((used >> b) & 1u) continue;
+                if (pass == 0) {
+                    unsigned v = v2_bank(b);
+                    for (int j = 3; j >= 0 && v; --j)
+                        if ((v >> j) & 1u) {
+                            if (!basis[j]) {
+                                basis[j] = v;
+                                break;
+                            }
+                            v ^= basis[j];
+                        }
+                    if (!v) continue;
+                }
+                rows[nr++] = b;
+                used |= 1u << b;
+            }
+        for (int b = 0; b < T; ++b)
+            if (!((used >> b) & 1u)) rows[nr++] = b;
+        uint32_t tpos = 0;
+        for (int i = 0; i < 7; ++i) tpos |= (uint32_t)rows[i] << (4 * i);
+        const int shift = cum > 1.0 ? std::min(100, (int)std::ceil(std::log2(cum))) : 0;
+        for (int x = g; x <= e; ++x) {
+            uint32_t rpos = 0;
+            int m = 0;
+            for (int b = 0; b < T; ++b)
+                if ((lmask[x] >> b) & 1u) rpos |= (uint32_t)b << (4 * m++);
+            for (int b = 0; b < T; ++b)
+                if (((local & ~lmask[x]) >> b) & 1u) rpos |= (uint32_t)b << (4 * m++);
+            gd[x].rpos = rpos;
+            gd[x].tpos = tpos;
+            gd[x].k = (gd[x].k & ~(kGateRunStart | kGateRunEnd | (0xff << kGateShiftBit))) | kGateV2;
+            gd[x].pair = 0;
+            std::memset(gd[x].xu, 0, sizeof gd[x].xu);
+        }
+        gd[g].k |= kGateRunStart | (shift << kGateShiftBit);
+        gd[e].k |= kGateRunEnd;
+        for (int x = g; x < e; ++x) {
+            // next gate's role r (config bit r < 4, group bit r - 4) -> column of this gate's D
+            for (int r = 0; r < 6; ++r) {
+                const uint32_t b = (gd[x + 1].rpos >> (4 * r)) & 15u;
+                uint16_t u = 0;
+                for (int q = 0; q < 6; ++q)
+                    if (((gd[x].rpos >> (4 * q)) & 15u) == b) u = (uint16_t)(q < 4 ? (2u << q) : (64u << (q - 4)));
+                gd[x].xu[r] = u;
+            }
+        }
+        g = e + 1;
+    }
+}
+
 }  // namespace
 
 qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const ObsGroups& og,
@@ -677,10 +769,10 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
                     const uint64_t pm = padded(g);
                     const int d = 1 << popc(pm);
                     // tensor cores: the GEMM operand, tc_gate_bytes(tc_k) bytes (complex64 units)
-                    gd.mat_off = alloc(P.tc ? tc_gate_bytes(P.tc_k) / 8 : d * d);
+                    gd.mat_off = alloc(P.v2 ? kV2GateBytes / 8 : (P.tc ? tc_gate_bytes(P.tc_k) / 8 : d * d));
                     FusedDesc fd;
                     fd.mat_off = gd.mat_off;
-                    fd.k = popc(pm) | (P.tc ? kGateTC : 0);
+                    fd.k = popc(pm) | (P.tc ? kGateTC : 0) | (P.v2 ? kGateV2 : 0);
                     fd.cons_begin = (int32_t)out.cons.size();
                     fd.cons_count = (int32_t)g.items.size();
                     for (int it : g.items) {
@@ -740,7 +832,18 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
                 const int R = (P.tc && P.tc_k == 6 && (gd.k & kGateTC)) ? 6 : P.R;
                 gate_layout(gate_masks[pd.gate_begin + g], pd.tile_mask, T, R, gd.rpos, gd.tpos);
             }
-            if (P.tc && P.tc_k == 4) {
+            if (P.v2) {
+                std::vector<uint32_t> lm(pd.gate_count);
+                for (int g = 0; g < pd.gate_count; ++g) {
+                    uint32_t l = 0;
+                    int i = 0;
+                    for (uint64_t mk = pd.tile_mask; mk; mk &= mk - 1, ++i)
+                        if ((gate_masks[pd.gate_begin + g] >> __builtin_ctzll(mk)) & 1u) l |= 1u << i;
+                    lm[g] = l;
+                }
+                v2_layouts(out.gates.data() + pd.gate_begin, lm.data(), gate_norms.data() + pd.gate_begin,
+                           pd.gate_count);
+            } else if (P.tc && P.tc_k == 4) {
                 tc_runs(out.gates.data() + pd.gate_begin, gate_norms.data() + pd.gate_begin, pd.gate_count, T,
                         out.fused, out.cons, gate_fused.data() + pd.gate_begin);
                 for (int g = 0; g < pd.gate_count; ++g)

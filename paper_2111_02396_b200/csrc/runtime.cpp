@@ -1088,3 +1088,37 @@ extern "C" qt_status qt_plan_bank_stats(qt_plan plan, uint64_t seed, uint64_t tr
     }
     return QT_OK;
 }
+
+// Diagnostic (undeclared, like qt_plan_bank_stats): the pass / fused-gate structure of
+// one trajectory's program.  out = [n_pass, then per pass: tile_mask, flags,
+// gate_count, then per gate: global qubit mask of its (padded) matrix bits, k].
+extern "C" qt_status qt_plan_dump(qt_plan plan, uint64_t seed, uint64_t traj, int64_t* out, int64_t cap) {
+    if (!plan || !out) return fail(QT_EINVAL, "NULL argument");
+    const Plan& P = plan_of(plan);
+    ObsGroups og;
+    og.ranges.push_back({0, 0});
+    og.masks.push_back(0);
+    TrajProgram pg;
+    qt_status e = plan_trajectory(P, seed, traj, og, pg);
+    if (e != QT_OK) return e;
+    int64_t w = 0;
+    auto put = [&](int64_t v) {
+        if (w < cap) out[w] = v;
+        ++w;
+    };
+    put((int64_t)pg.passes.size());
+    for (const PassDesc& ps : pg.passes) {
+        put((int64_t)ps.tile_mask);
+        put(ps.flags);
+        put(ps.gate_count);
+        for (int g = 0; g < ps.gate_count; ++g) {
+            const GateDesc& G = pg.gates[ps.gate_begin + g];
+            const int k = (G.k & kGateTC) ? 4 : (G.k & 0xff);
+            uint64_t m = 0;
+            for (int j = 0; j < k; ++j) m |= 1ull << ps.tq[(G.rpos >> (4 * j)) & 15u];
+            put((int64_t)m);
+            put(G.k);
+        }
+    }
+    return w <= cap ? QT_OK : fail(QT_EINVAL, "plan dump: capacity too small");
+}
