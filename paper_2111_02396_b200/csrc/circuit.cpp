@@ -476,11 +476,11 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
         P.R = 5;
         P.f = f;
         P.tc_k = f <= 4 ? 4 : f;
-        // T = 13: 128 threads per compute warpgroup hold 64 amplitudes each for the
+        // T = 13: 256 threads per compute warpgroup hold 32 amplitudes each for the
         // CUDA-core gates (device-chosen conventional operators)
         if (P.T == 13) {
             P.v2 = true;
-            P.R = 6;
+            P.R = 5;
         }
     }
     // canonical order: moment ascending, then call order (stable)

@@ -27,9 +27,9 @@ struct PassDesc {
     int32_t obs_count;
     uint8_t tq[16];       // global qubit of tile bit i (ascending), i < T
     int32_t slot;         // batch slot (set by the executor in the per-step launch arrays)
-    int32_t pad;
+    int32_t pad[3];
 };
-static_assert(sizeof(PassDesc) == 56, "PassDesc layout");
+static_assert(sizeof(PassDesc) == 64, "PassDesc layout");
 
 // A fused gate inside a pass and the register layout used to apply it:
 // register bit m of a thread's 2^R amplitudes <-> tile-local bit rpos[m]
@@ -71,8 +71,19 @@ constexpr int kGateShiftBit = 16;         // bits 16..23: run scale headroom (lo
 //   kGateRunStart: gather the fp32 tile into TMEM operand A (new f16 tile scale);
 //   kGateRunEnd: write D back to the fp32 tile; otherwise xu[0..5] = TMEM column
 //   offset, in this gate's D, of the next gate's config bits 0..3 / group bits 0..1.
+//   The 40 bytes after `k` of a v2 gate are 20 uint16 (v2_units): [0..3] fp32-tile byte
+//   offsets of the config bits, [4..5] of the group bits, [6..12] of the row bits
+//   (TMEM lane bits 0..4, warp bits 0..1), [13..18] = xu (next-gate source columns).
 constexpr int32_t kGateV2 = 0x800;
+#ifdef __CUDACC__
+#define QT_HD __host__ __device__
+#else
+#define QT_HD
+#endif
+QT_HD inline uint16_t* v2_units(GateDesc& g) { return reinterpret_cast<uint16_t*>(&g.rpos); }
+QT_HD inline const uint16_t* v2_units(const GateDesc& g) { return reinterpret_cast<const uint16_t*>(&g.rpos); }
 constexpr int32_t kGateRunEnd = 0x1000;
+constexpr int32_t kGateXNext = 0x2000;  // v2: the transition to the next gate is an X (16x256b) transposition
 // Pool bytes of a v2 gate operand: B = 32 rows x [W_hi (32 f16) | W_lo (32 f16)], SWIZZLE_128B.
 constexpr int kV2GateBytes = 4096;
 // Pool bytes of a tensor-core gate operand padded to k qubits (tc_common.cuh

@@ -551,79 +551,199 @@ inline unsigned v2_bank(int b) {  // slot bits 0..3 of tile bit b under the T = 
 }
 }  // namespace
 
-void v2_layouts(GateDesc* gd, const uint32_t* lmask, const double* norms, int count) {
+// Layout roles of a v2 gate: the tile bits of its matrix bits (cfg, in matrix-bit
+// order), of its two group bits, of the 5 TMEM lane bits and of the 2 warp bits.
+struct V2Lay {
+    int cfg[4], grp[2], lane[5], warp[2];
+};
+
+void v2_layouts(GateDesc* gd, const uint32_t* lmask, const double* norms, int count, std::vector<FusedDesc>& fused,
+                std::vector<ConsDesc>& cons, const int* gate_fused) {
     constexpr int T = 13;
-    for (int g = 0; g < count;) {
-        if (!(gd[g].k & kGateTC)) {
-            ++g;
+    constexpr int kNever = 1 << 20;
+    auto bits_of = [](uint32_t m, int* out) {
+        int k = 0;
+        for (int b = 0; b < 13; ++b)
+            if ((m >> b) & 1u) out[k++] = b;
+        return k;
+    };
+    // first gate index > i that uses tile bit b (tensor-core gates of this pass)
+    auto next_use = [&](int i, int b) {
+        for (int j = i + 1; j < count; ++j) {
+            if (!(gd[j].k & kGateTC)) break;
+            if ((lmask[j] >> b) & 1u) return j;
+        }
+        return kNever;
+    };
+    // matrix-bit order of gate i's qubits: `first` (or -1) fixed at bit 0, then the
+    // qubits needed latest at bits 0 / 1 (they leave for lane bits at an X transition),
+    // the ones needed soonest at bits 2 / 3
+    auto order_cfg = [&](int i, int first, int* cfg) {
+        int q[4];
+        bits_of(lmask[i], q);
+        int rest[4], nr = 0;
+        for (int t = 0; t < 4; ++t)
+            if (q[t] != first) rest[nr++] = q[t];
+        std::stable_sort(rest, rest + nr, [&](int a, int b) { return next_use(i, a) > next_use(i, b); });
+        int m = 0;
+        if (first >= 0) cfg[m++] = first;
+        for (int t = 0; t < nr; ++t) cfg[m++] = rest[t];
+    };
+    // fresh layout of gate i (segment start: gathered from the fp32 tile)
+    auto fresh = [&](int i, V2Lay& L) {
+        order_cfg(i, -1, L.cfg);
+        // tile bits not in gate i, in order of next use
+        int fut[13], nf = 0;
+        for (int b = 0; b < T; ++b)
+            if (!((lmask[i] >> b) & 1u)) fut[nf++] = b;
+        std::stable_sort(fut, fut + nf, [&](int a, int b) { return next_use(i, a) < next_use(i, b); });
+        // group bits: the two needed soonest (local transitions); then lane bits by
+        // arrival through X transitions (L3, L4 next, L1, L2 after one X, L0 after
+        // two); the bits never needed are warp bits
+        L.grp[0] = fut[0];
+        L.grp[1] = fut[1];
+        static const int lane_order[5] = {3, 4, 1, 2, 0};
+        for (int t = 0; t < 5; ++t) L.lane[lane_order[t]] = fut[2 + t];
+        L.warp[0] = fut[7];
+        L.warp[1] = fut[8];
+        // bank-conflict-free gathers want tile bit 0 in lane bit 0 when it is a lane
+        // bit at all (the other low lane bits keep their arrival order)
+    };
+    auto local_of = [](const V2Lay& L) {
+        uint32_t m = 0;
+        for (int t = 0; t < 4; ++t) m |= 1u << L.cfg[t];
+        for (int t = 0; t < 2; ++t) m |= 1u << L.grp[t];
+        return m;
+    };
+    auto unit = [](uint32_t b) -> uint16_t {
+        const uint32_t L = 1u << b;
+        return (uint16_t)((L ^ ((((L >> 4) ^ (L >> 7) ^ (L >> 10)) & 7u) << 1)) << 3);
+    };
+    std::vector<V2Lay> lay(count);
+    std::vector<int> tr(count, 0);  // transition into gate i: 0 start (gather), 1 L, 2 X
+    double cum = 1.0;
+    for (int i = 0; i < count; ++i) {
+        if (!(gd[i].k & kGateTC)) {
+            cum = 1.0;
             continue;
         }
-        // segment [g, e]: union of the gates' tile bits <= 6, norm product <= 16
-        uint32_t local = lmask[g];
-        double cum = norms[g];
-        int e = g;
-        while (e + 1 < count && (gd[e + 1].k & kGateTC) && __builtin_popcount(local | lmask[e + 1]) <= 6 &&
-               cum * norms[e + 1] <= 16.0) {
-            ++e;
-            local |= lmask[e];
-            cum *= norms[e];
-        }
-        // pad the thread-local set to 6 bits with the highest free tile bits (the low
-        // ones stay lane bits: bank-conflict-free gathers)
-        for (int b = T - 1; b >= 0 && __builtin_popcount(local) < 6; --b) local |= 1u << b;
-        // lane bits 0..3: GF(2)-independent bank vectors first (tile bit 0 first)
-        int rows[7], nr = 0;
-        unsigned basis[4] = {0, 0, 0, 0};
-        uint32_t used = local;
-        for (int pass = 0; pass < 2; ++pass)
-            for (int b = 0; b < T && nr < 4; ++b) {
-                if ((used >> b) & 1u) continue;
-                if (pass == 0) {
-                    unsigned v = v2_bank(b);
-                    for (int j = 3; j >= 0 && v; --j)
-                        if ((v >> j) & 1u) {
-                            if (!basis[j]) {
-                                basis[j] = v;
-                                break;
-                            }
-                            v ^= basis[j];
-                        }
-                    if (!v) continue;
+        const bool prev_tc = i > 0 && (gd[i - 1].k & kGateTC);
+        int t = 0;
+        if (prev_tc && cum * norms[i] <= 16.0) {
+            const V2Lay& P = lay[i - 1];
+            const uint32_t local = local_of(P);
+            if ((lmask[i] & ~local) == 0) {
+                t = 1;  // L: same rows, new roles of the 6 thread-local bits
+                V2Lay& L = lay[i];
+                order_cfg(i, -1, L.cfg);
+                int g2[6], ng2 = 0;
+                for (int b = 0; b < T; ++b)
+                    if (((local & ~lmask[i]) >> b) & 1u) g2[ng2++] = b;
+                L.grp[0] = g2[0];
+                L.grp[1] = g2[1];
+                std::memcpy(L.lane, P.lane, sizeof L.lane);
+                std::memcpy(L.warp, P.warp, sizeof L.warp);
+            } else {
+                // X: rows (c0, c1, L0, L1, L2 | warps); local = {L3, L4, c2, c3, j0, j1}
+                const uint32_t lx = (1u << P.lane[3]) | (1u << P.lane[4]) | (1u << P.cfg[2]) | (1u << P.cfg[3]) |
+                                    (1u << P.grp[0]) | (1u << P.grp[1]);
+                if ((lmask[i] & ~lx) == 0 && ((lmask[i] >> P.lane[3]) & 1u)) {
+                    t = 2;
+                    V2Lay& L = lay[i];
+                    order_cfg(i, P.lane[3], L.cfg);
+                    int g2[6], ng2 = 0;
+                    for (int b = 0; b < T; ++b)
+                        if (((lx & ~lmask[i]) >> b) & 1u) g2[ng2++] = b;
+                    L.grp[0] = g2[0];
+                    L.grp[1] = g2[1];
+                    L.lane[0] = P.cfg[0];
+                    L.lane[1] = P.cfg[1];
+                    L.lane[2] = P.lane[0];
+                    L.lane[3] = P.lane[1];
+                    L.lane[4] = P.lane[2];
+                    L.warp[0] = P.warp[0];
+                    L.warp[1] = P.warp[1];
                 }
-                rows[nr++] = b;
-                used |= 1u << b;
-            }
-        for (int b = 0; b < T; ++b)
-            if (!((used >> b) & 1u)) rows[nr++] = b;
-        uint32_t tpos = 0;
-        for (int i = 0; i < 7; ++i) tpos |= (uint32_t)rows[i] << (4 * i);
-        const int shift = cum > 1.0 ? std::min(100, (int)std::ceil(std::log2(cum))) : 0;
-        for (int x = g; x <= e; ++x) {
-            uint32_t rpos = 0;
-            int m = 0;
-            for (int b = 0; b < T; ++b)
-                if ((lmask[x] >> b) & 1u) rpos |= (uint32_t)b << (4 * m++);
-            for (int b = 0; b < T; ++b)
-                if (((local & ~lmask[x]) >> b) & 1u) rpos |= (uint32_t)b << (4 * m++);
-            gd[x].rpos = rpos;
-            gd[x].tpos = tpos;
-            gd[x].k = (gd[x].k & ~(kGateRunStart | kGateRunEnd | (0xff << kGateShiftBit))) | kGateV2;
-            gd[x].pair = 0;
-            std::memset(gd[x].xu, 0, sizeof gd[x].xu);
-        }
-        gd[g].k |= kGateRunStart | (shift << kGateShiftBit);
-        gd[e].k |= kGateRunEnd;
-        for (int x = g; x < e; ++x) {
-            // next gate's role r (config bit r < 4, group bit r - 4) -> column of this gate's D
-            for (int r = 0; r < 6; ++r) {
-                const uint32_t b = (gd[x + 1].rpos >> (4 * r)) & 15u;
-                uint16_t u = 0;
-                for (int q = 0; q < 6; ++q)
-                    if (((gd[x].rpos >> (4 * q)) & 15u) == b) u = (uint16_t)(q < 4 ? (2u << q) : (64u << (q - 4)));
-                gd[x].xu[r] = u;
             }
         }
-        g = e + 1;
+        if (t == 0) {
+            fresh(i, lay[i]);
+            cum = 1.0;
+        }
+        cum *= norms[i];
+        tr[i] = t;
+    }
+    // segments = maximal runs of gates joined by L / X transitions; the scale headroom
+    // of a segment covers the product of its gates' norm bounds
+    for (int i = 0; i < count; ++i) {
+        if (!(gd[i].k & kGateTC)) continue;
+        const V2Lay& L = lay[i];
+        const bool start = tr[i] == 0;
+        const bool end = i + 1 >= count || !(gd[i + 1].k & kGateTC) || tr[i + 1] == 0;
+        int32_t k = (gd[i].k & ~(kGateRunStart | kGateRunEnd | kGateXNext | (0xff << kGateShiftBit))) | kGateV2;
+        if (start) {
+            double c = 1.0;
+            for (int j = i; j < count && (gd[j].k & kGateTC) && (j == i || tr[j] != 0); ++j) c *= norms[j];
+            const int shift = c > 1.0 ? std::min(100, (int)std::ceil(std::log2(c))) : 0;
+            k |= kGateRunStart | (shift << kGateShiftBit);
+        }
+        if (end) k |= kGateRunEnd;
+        if (!end && tr[i + 1] == 2) k |= kGateXNext;
+        uint16_t u[20] = {0};
+        for (int r = 0; r < 4; ++r) u[r] = unit((uint32_t)L.cfg[r]);
+        for (int r = 0; r < 2; ++r) u[4 + r] = unit((uint32_t)L.grp[r]);
+        for (int r = 0; r < 5; ++r) u[6 + r] = unit((uint32_t)L.lane[r]);
+        for (int r = 0; r < 2; ++r) u[11 + r] = unit((uint32_t)L.warp[r]);
+        if (!end) {
+            const V2Lay& N = lay[i + 1];
+            if (tr[i + 1] == 1) {
+                // L: TMEM column (in this gate's D) of the next gate's roles cfg0..3, grp0..1
+                const int roles[6] = {N.cfg[0], N.cfg[1], N.cfg[2], N.cfg[3], N.grp[0], N.grp[1]};
+                for (int r = 0; r < 6; ++r) {
+                    uint16_t v = 0;
+                    for (int q = 0; q < 4; ++q)
+                        if (L.cfg[q] == roles[r]) v = (uint16_t)(2u << q);
+                    for (int q = 0; q < 2; ++q)
+                        if (L.grp[q] == roles[r]) v = (uint16_t)(64u << q);
+                    u[13 + r] = v;
+                }
+            } else {
+                // X: 16x256b loads; the next gate's matrix bit 0 is this gate's lane bit 3
+                // (load register pair), roles cfg1..3, grp0..1 -> TMEM address deltas of
+                // lane bit 4 (lane + 16), config bits 2, 3 (columns 8, 16), groups (64, 128)
+                const int roles[5] = {N.cfg[1], N.cfg[2], N.cfg[3], N.grp[0], N.grp[1]};
+                for (int r = 0; r < 5; ++r) {
+                    uint16_t v = 0;
+                    if (roles[r] == L.lane[4]) v = 0x8000u;  // lane + 16 (the kernel expands it)
+                    if (roles[r] == L.cfg[2]) v = 8;
+                    if (roles[r] == L.cfg[3]) v = 16;
+                    if (roles[r] == L.grp[0]) v = 64;
+                    if (roles[r] == L.grp[1]) v = 128;
+                    u[14 + r] = v;
+                }
+            }
+        }
+        gd[i].k = k;
+        gd[i].mat_off = gd[i].mat_off;
+        std::memcpy(v2_units(gd[i]), u, sizeof u);
+        // matrix bit m <-> tile bit cfg[m]: constituent positions follow that order
+        if (gate_fused[i] >= 0) {
+            int asc[4];
+            bits_of(lmask[i], asc);
+            int rank_to_m[4];
+            for (int a = 0; a < 4; ++a)
+                for (int m = 0; m < 4; ++m)
+                    if (L.cfg[m] == asc[a]) rank_to_m[a] = m;
+            const FusedDesc& fd = fused[gate_fused[i]];
+            for (int ci = fd.cons_begin; ci < fd.cons_begin + fd.cons_count; ++ci) {
+                uint32_t pos = cons[ci].pos, np = pos;
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t pv = (pos >> (4 * j)) & 15u;
+                    if (pv < 4) np = (np & ~(15u << (4 * j))) | ((uint32_t)rank_to_m[pv] << (4 * j));
+                }
+                cons[ci].pos = np;
+            }
+        }
     }
 }
 
@@ -842,7 +962,7 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
                     lm[g] = l;
                 }
                 v2_layouts(out.gates.data() + pd.gate_begin, lm.data(), gate_norms.data() + pd.gate_begin,
-                           pd.gate_count);
+                           pd.gate_count, out.fused, out.cons, gate_fused.data() + pd.gate_begin);
             } else if (P.tc && P.tc_k == 4) {
                 tc_runs(out.gates.data() + pd.gate_begin, gate_norms.data() + pd.gate_begin, pd.gate_count, T,
                         out.fused, out.cons, gate_fused.data() + pd.gate_begin);

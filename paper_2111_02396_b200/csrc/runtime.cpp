@@ -774,7 +774,10 @@ static qt_status run_single(qt_ctx ctx, qt_plan plan, float2* state, const ObsGr
     }
     for (int rep = 0; rep < std::max(repeats, 1); ++rep) {
         if (kernel_ms && rep == 1) QT_CK(cudaEventRecord(e0, s));  // rep 0 = warm-up
-        for (int step = 0; step < np; ++step) QT_CK(launch_tile_pass(A, P.R, P.tc ? P.tc_k : 0, step, ntiles, 1, s));
+        for (int step = 0; step < np; ++step) {
+            A.step_passes = B.passes.as<PassDesc>() + step;  // one slot: its pass of this step (slot 0)
+            QT_CK(launch_tile_pass(A, P.R, P.tc ? P.tc_k : 0, step, ntiles, 1, s));
+        }
     }
     if (kernel_ms) {
         if (repeats <= 1) QT_CK(cudaEventRecord(e0, s));
@@ -1115,7 +1118,11 @@ extern "C" qt_status qt_plan_dump(qt_plan plan, uint64_t seed, uint64_t traj, in
             const GateDesc& G = pg.gates[ps.gate_begin + g];
             const int k = (G.k & kGateTC) ? 4 : (G.k & 0xff);
             uint64_t m = 0;
-            for (int j = 0; j < k; ++j) m |= 1ull << ps.tq[(G.rpos >> (4 * j)) & 15u];
+            if (G.k & kGateV2) {  // v2 units: fp32 byte offset of a tile bit b has its top bit at b + 3
+                for (int j = 0; j < 4; ++j) m |= 1ull << ps.tq[31 - __builtin_clz((uint32_t)v2_units(G)[j]) - 3];
+            } else {
+                for (int j = 0; j < k; ++j) m |= 1ull << ps.tq[(G.rpos >> (4 * j)) & 15u];
+            }
             put((int64_t)m);
             put(G.k);
         }

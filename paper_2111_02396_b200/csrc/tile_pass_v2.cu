@@ -31,12 +31,23 @@ constexpr int TILE = 1 << T;
 constexpr uint32_t kTileBytes = TILE * 8;  // 64 KB
 constexpr int NBUF = 3;
 constexpr int NWG = 2;
-constexpr int NT = 128;  // threads per compute warpgroup
-constexpr int NA = TILE / NT;  // 64 amplitudes per thread
-constexpr int kThreads = (4 * NWG + 1) * 32;
+constexpr int NT = 256;        // threads per compute warpgroup: 2 warps per TMEM lane quarter
+constexpr int NWW = NT / 32;   // warps per warpgroup
+constexpr int NA = TILE / NT;  // 32 amplitudes per thread
+constexpr int kThreads = NWG * NT;
 constexpr uint32_t kWOff = NBUF * kTileBytes;
-constexpr uint32_t kRedOff = kWOff + NWG * 2 * kV2GateBytes;
-constexpr uint32_t kMbarOff = kRedOff + NWG * 64 * 8;
+// per-warpgroup item contexts, double-buffered: item k of a warpgroup uses ctx[k & 1],
+// prepared (descriptors, tile bases) while item k - 1 runs
+struct alignas(16) Ctx {
+    PassDesc p;       // the item's pass
+    PassDesc p3;      // pass of the item this warpgroup loads when the item is done
+    uint64_t base;    // global index of the tile's amplitude 0
+    uint64_t base3;   // same for the item loaded at the end
+    GateDesc g[kMaxPassGates];
+};
+constexpr uint32_t kCtxOff = kWOff + NWG * 2 * kV2GateBytes;
+constexpr uint32_t kRedOff = kCtxOff + NWG * 2 * sizeof(Ctx);
+constexpr uint32_t kMbarOff = kRedOff + NWG * 256 * 8;
 constexpr uint32_t kMiscOff = kMbarOff + 16 * 8;
 constexpr size_t kSmemBytes = kMiscOff + 64 + 1024;  // + alignment slack
 
@@ -48,12 +59,19 @@ __device__ __forceinline__ void bar_wg(int wg) {
     asm volatile("bar.sync %0, %1;\n" ::"r"(1 + wg), "r"(NT) : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait_s(uint32_t a, uint32_t phase) {
+__device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t phase) {
+    uint32_t ok;
     asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(a), "r"(phase) : "memory");
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(ok) : "r"(a), "r"(phase) : "memory");
+    return ok != 0;
+}
+// wait with a short sleep between polls (the spinning warps would otherwise take
+// issue slots from the other warpgroup)
+__device__ __forceinline__ void mbar_wait_s(uint32_t a, uint32_t phase) {
+    while (!mbar_try(a, phase)) __nanosleep(64);
 }
 __device__ __forceinline__ void mbar_init_s(uint32_t a, uint32_t c) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(c) : "memory");
@@ -83,19 +101,57 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint3
 __device__ __forceinline__ void tmem_ld2(uint32_t taddr, uint32_t& a, uint32_t& b) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];\n" : "=r"(a), "=r"(b) : "r"(taddr) : "memory");
 }
+// 16 lanes x 256 bits: thread t receives lane base + t/4 (r0, r1) and base + 8 + t/4 (r2,
+// r3), columns 2 (t % 4) (r0, r2) and 2 (t % 4) + 1 (r1, r3) -- measured, profiles/r2_tmem_shapes.txt
+__device__ __forceinline__ void tmem_ld_16x256(uint32_t taddr, uint32_t (&r)[4]) {
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(taddr) : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+        "%13, %14, %15, %16};\n" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
 
-// f16 hi / lo split of a scaled complex amplitude: hi = x with the 13 low mantissa
-// bits cleared (exact in f16 above 2^-14), lo = the remainder rounded to f16.
-__device__ __forceinline__ void split(float re, float im, uint32_t& hi, uint32_t& lo) {
-    const float hr = __uint_as_float(__float_as_uint(re) & 0xFFFFE000u);
-    const float hm = __uint_as_float(__float_as_uint(im) & 0xFFFFE000u);
+// Packed fp32 pair arithmetic (sm_100 FADD2 / FMUL2).
+__device__ __forceinline__ uint64_t pk2(float x, float y) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+    return r;
+}
+__device__ __forceinline__ float2 upk2(uint64_t r) {
+    float2 o;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+    return o;
+}
+__device__ __forceinline__ uint64_t sub2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+// f16 hi / lo split of a scaled complex amplitude (packed fp32 pair): hi = x with the
+// 13 low mantissa bits cleared (exact in f16 above 2^-14), lo = the remainder rounded.
+__device__ __forceinline__ void split(uint64_t x, uint32_t& hi, uint32_t& lo) {
+    const float2 xf = upk2(x);
+    const float hr = __uint_as_float(__float_as_uint(xf.x) & 0xFFFFE000u);
+    const float hm = __uint_as_float(__float_as_uint(xf.y) & 0xFFFFE000u);
+    const float2 l = upk2(sub2(x, pk2(hr, hm)));
     const __half2 h2 = __floats2half2_rn(hr, hm);
-    const __half2 l2 = __floats2half2_rn(re - hr, im - hm);
+    const __half2 l2 = __floats2half2_rn(l.x, l.y);
     hi = *reinterpret_cast<const uint32_t*>(&h2);
     lo = *reinterpret_cast<const uint32_t*>(&l2);
 }
 
-// Deterministic warpgroup sums (fixed order: lanes by xor tree, then warps 0..3).
+// Deterministic warpgroup sums (fixed order: lanes by xor tree, then warps 0..7).
 template <int N>
 __device__ __forceinline__ void wg_sum_n(double (&v)[N], double* red, int wg) {
     const int wtid = threadIdx.x & (NT - 1);
@@ -103,7 +159,7 @@ __device__ __forceinline__ void wg_sum_n(double (&v)[N], double* red, int wg) {
     for (int i = 0; i < N; ++i)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
-    constexpr int C = 16;  // values per chunk (red: 64 doubles = 4 warps x 16)
+    constexpr int C = 16;  // values per chunk (red: 128 doubles = 8 warps x 16)
 #pragma unroll
     for (int c0 = 0; c0 < N; c0 += C) {
         bar_wg(wg);
@@ -112,7 +168,12 @@ __device__ __forceinline__ void wg_sum_n(double (&v)[N], double* red, int wg) {
             for (int i = c0; i < N && i < c0 + C; ++i) red[(wtid >> 5) * C + (i - c0)] = v[i];
         bar_wg(wg);
 #pragma unroll
-        for (int i = c0; i < N && i < c0 + C; ++i) v[i] = red[i - c0] + red[C + i - c0] + red[2 * C + i - c0] + red[3 * C + i - c0];
+        for (int i = c0; i < N && i < c0 + C; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < NWW; ++w) s += red[w * C + i - c0];
+            v[i] = s;
+        }
     }
 }
 
@@ -187,19 +248,13 @@ struct Item {
     uint32_t tile;
 };
 
-// Item i of the step: slot index i >> tshift, tile i & (ntiles - 1); nullptr pass =
-// the slot has no pass at this step (slot-table launches).
-__device__ __forceinline__ Item item_of(const TileArgs& A, int step, uint32_t i, int tshift) {
+// Item i of the step: the pass of active slot i >> tshift (the executor's per-step
+// array), tile i & (ntiles - 1).
+__device__ __forceinline__ Item item_of(const TileArgs& A, uint32_t i, int tshift) {
     Item it;
-    const int si = (int)(i >> tshift);
+    it.p = A.step_passes + (i >> tshift);
+    it.slot = it.p->slot;
     it.tile = i & ((1u << tshift) - 1u);
-    if (A.step_passes) {
-        it.p = A.step_passes + si;
-        it.slot = it.p->slot;
-    } else {
-        it.slot = si;
-        it.p = step < A.pass_count[si] ? A.passes + A.pass_start[si] + step : nullptr;
-    }
     return it;
 }
 
@@ -214,6 +269,40 @@ __device__ __forceinline__ uint64_t tile_base(const PassDesc& P, uint32_t tile) 
     return base;
 }
 
+// fp32-tile byte offsets of a gate layout (desc.hpp v2_units): this thread's row
+// (lane bits + warp bits) with its group 2h (base0) or 2h + 1 (base1), and the 16
+// configurations as base ^ c01[c & 3] ^ c23[c >> 2] (one 3-input XOR per access).
+struct Fp32Layout {
+    uint32_t base0, base1;
+    uint32_t c01[4], c23[4];
+};
+__device__ __forceinline__ Fp32Layout fp32_layout(const GateDesc& G, int wtid) {
+    const uint16_t* u = v2_units(G);
+    // (u is 8-byte aligned: GateDesc::rpos sits at offset 8)
+    const uint2 w0 = *reinterpret_cast<const uint2*>(u), w1 = *reinterpret_cast<const uint2*>(u + 4);
+    const uint2 w2 = *reinterpret_cast<const uint2*>(u + 8), w3 = *reinterpret_cast<const uint2*>(u + 12);
+    const uint32_t uc0 = w0.x & 0xffffu, uc1 = w0.x >> 16, uc2 = w0.y & 0xffffu, uc3 = w0.y >> 16;
+    const uint32_t ug0 = w1.x & 0xffffu, ug1 = w1.x >> 16;
+    const uint32_t ur[7] = {w1.y & 0xffffu, w1.y >> 16, w2.x & 0xffffu, w2.x >> 16, w2.y & 0xffffu, w2.y >> 16,
+                            w3.x & 0xffffu};
+    Fp32Layout L;
+    uint32_t rb = 0;
+#pragma unroll
+    for (int q = 0; q < 7; ++q)
+        if ((wtid >> q) & 1) rb ^= ur[q];
+    L.base0 = rb ^ ((wtid >> 7) ? ug1 : 0u);
+    L.base1 = L.base0 ^ ug0;
+    L.c01[0] = 0;
+    L.c01[1] = uc0;
+    L.c01[2] = uc1;
+    L.c01[3] = uc0 ^ uc1;
+    L.c23[0] = 0;
+    L.c23[1] = uc2;
+    L.c23[2] = uc3;
+    L.c23[3] = uc2 ^ uc3;
+    return L;
+}
+
 __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArgs A, const int step,
                                                                     const uint32_t nitems, const int tshift) {
     extern __shared__ unsigned char smem_raw[];
@@ -223,22 +312,16 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t mb = sm_s + kMbarOff;  // full[3], empty[3], mma[2], wfull[2][2]
     auto full_bar = [&](int b) { return mb + 8u * (uint32_t)b; };
-    auto empty_bar = [&](int b) { return mb + 8u * (uint32_t)(3 + b); };
     auto mma_bar = [&](int w) { return mb + 8u * (uint32_t)(6 + w); };
     auto wfull_bar = [&](int w, int i) { return mb + 8u * (uint32_t)(8 + 2 * w + i); };
     uint32_t* misc = reinterpret_cast<uint32_t*>(sm + kMiscOff);  // [0] tmem base, [1..2] last flags
-    if (warp == 0) {
-        tc::tmem_alloc(misc, 512);
-    }
+    if (warp == 0) tc::tmem_alloc(misc, 512);
     if (tid == 32) {
-        for (int b = 0; b < NBUF; ++b) {
-            mbar_init_s(full_bar(b), 32);
-            mbar_init_s(empty_bar(b), 1);
-        }
+        for (int b = 0; b < NBUF; ++b) mbar_init_s(full_bar(b), NT);
         for (int w = 0; w < NWG; ++w) {
-            mbar_init_s(mma_bar(w), 1);
-            mbar_init_s(wfull_bar(w, 0), 1);
-            mbar_init_s(wfull_bar(w, 1), 1);
+            mbar_init_s(mma_bar(w), 4);  // one commit per issuing warp
+            mbar_init_s(wfull_bar(w, 0), NT);
+            mbar_init_s(wfull_bar(w, 1), NT);
         }
         tc::fence_mbar_init();
     }
@@ -249,256 +332,340 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
     const int n = A.n;
     const uint32_t ntiles = 1u << tshift;
 
-    if (warp == 4 * NWG) {
-        // ---------------- loader ----------------
-        int j = 0;
-        for (uint32_t i = blockIdx.x; i < nitems; i += gridDim.x) {
-            const Item it = item_of(A, step, i, tshift);
-            if (!it.p) continue;
-            const int b = j % NBUF;
-            if (j >= NBUF) mbar_wait_s(empty_bar(b), (uint32_t)((j / NBUF - 1) & 1));
-            const PassDesc& P = *it.p;
-            const uint32_t buf = sm_s + (uint32_t)b * kTileBytes;
-            if (P.flags & kPassInit) {
-                // first pass of a trajectory: |0...0> (amplitude 0 lives in tile 0, slot 0)
-                float4* t4 = reinterpret_cast<float4*>(sm + (size_t)b * kTileBytes);
-                for (int k = lane; k < TILE / 2; k += 32) t4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-                __syncwarp();
-                if (lane == 0 && it.tile == 0) t4[0] = make_float4(1.f, 0.f, 0.f, 0.f);
-                mbar_arrive_s(full_bar(b));
-            } else {
-                const float2* st = A.state + ((uint64_t)it.slot << n) + tile_base(P, it.tile);
-                // lane: pair p = lane & 7 of run h = 4 it + (lane >> 3); h bits 0, 1 fixed
-                const int p = lane & 7;
-                const uint32_t h0 = (uint32_t)(lane >> 3);
-                const uint64_t ofix = ((uint64_t)(h0 & 1u) << P.tq[4]) | ((uint64_t)(h0 >> 1) << P.tq[5]);
-                uint64_t M = 0;
+    // Tile loads: the warpgroup that releases a buffer loads its next occupant (item
+    // j + NBUF, processed by either warpgroup): 16-byte cp.async per thread, completing
+    // on the buffer's "full" mbarrier (NT arrivals).
+    auto load_item = [&](int jj, const PassDesc& P, uint32_t tile, uint64_t tbase_g, int wtid) {
+        const int b = jj % NBUF;
+        const uint32_t buf = sm_s + (uint32_t)b * kTileBytes;
+        if (P.flags & kPassInit) {
+            // first pass of a trajectory: |0...0> (amplitude 0 lives in tile 0, slot 0)
+            float4* t4 = reinterpret_cast<float4*>(sm + (size_t)b * kTileBytes);
+            for (int k = wtid; k < TILE / 2; k += NT)
+                t4[k] = make_float4((k == 0 && tile == 0) ? 1.f : 0.f, 0.f, 0.f, 0.f);
+            mbar_arrive_s(full_bar(b));
+        } else {
+            const float2* st = A.state + ((uint64_t)P.slot << n) + tbase_g;
+            // thread: pair p = wtid & 7 of run h = 32 k + (wtid >> 3); h bits 0..4 fixed
+            const int p = wtid & 7;
+            const uint32_t h0 = (uint32_t)(wtid >> 3);
+            uint64_t ofix = 0;
 #pragma unroll
-                for (int q = 6; q < T; ++q) M |= 1ull << P.tq[q];
-                uint64_t x = 0;
-                const float2* src = st + ofix + 2 * p;
-#pragma unroll 4
-                for (uint32_t k = 0; k < 128; ++k) {
-                    const uint32_t h = 4u * k + h0;
-                    const uint32_t L = 16u * h;
-                    const uint32_t slot = (L ^ ((((L >> 4) ^ (L >> 7) ^ (L >> 10)) & 7u) << 1)) ^ (2u * (uint32_t)p);
-                    cp_async16_s(buf + 8u * slot, src + x);
-                    x = (x - M) & M;
-                }
-                cp_async_arrive_noinc(full_bar(b));
+            for (int q = 0; q < 5; ++q) ofix |= (uint64_t)((h0 >> q) & 1u) << P.tq[4 + q];
+            // run offsets of tile bits 9..12 (k bits): sums of four basis offsets
+            const float2* src = st + ofix + 2 * p;
+            const float2* s1 = src + (1ull << P.tq[9]);
+            const uint64_t e1 = 1ull << P.tq[10], e2 = 1ull << P.tq[11], e3 = 1ull << P.tq[12];
+#pragma unroll
+            for (uint32_t k = 0; k < 16; ++k) {
+                const uint32_t L = 16u * (32u * k + h0);
+                const uint32_t slot = (L ^ ((((L >> 4) ^ (L >> 7) ^ (L >> 10)) & 7u) << 1)) ^ (2u * (uint32_t)p);
+                const uint64_t x = ((k & 2) ? e1 : 0ull) + ((k & 4) ? e2 : 0ull) + ((k & 8) ? e3 : 0ull);
+                cp_async16_s(buf + 8u * slot, ((k & 1) ? s1 : src) + x);
             }
-            ++j;
+            cp_async_arrive_noinc(full_bar(b));
         }
-        asm volatile("cp.async.wait_all;\n" ::: "memory");
-    } else {
+    };
+    {
         // ---------------- compute warpgroups ----------------
-        const int wg = warp >> 2;
+        const int wg = warp / NWW;
         const int wtid = tid & (NT - 1);
+        const int half = wtid >> 7;  // groups 2 half, 2 half + 1
         const uint32_t tbase = tmem + 256u * (uint32_t)wg;
         const uint32_t lane_off = ((uint32_t)(warp & 3) * 32u) << 16;
         const uint32_t tl = tbase + lane_off;  // this thread's TMEM lane, column 0 of the warpgroup
-        double* red = reinterpret_cast<double*>(sm + kRedOff) + 64 * wg;
+        const uint32_t tlh = tl + 128u * (uint32_t)half;  // its first group's D
+        double* red = reinterpret_cast<double*>(sm + kRedOff) + 256 * wg;
+        Ctx* ctxs = reinterpret_cast<Ctx*>(sm + kCtxOff) + 2 * wg;
         const uint32_t wbuf = sm_s + kWOff + (uint32_t)wg * 2u * kV2GateBytes;
         const bool elect = wtid == 0;
+        const bool issuer = (wtid & 31) == 0 && wtid < 128;  // MMA issue: lane 0 of warps 0..3 (group = warp)
+        const bool prep_warp = (wtid >> 5) == 1;  // warp 1 of the warpgroup prepares the next item's context
         uint32_t mma_phase = 0;
         uint32_t w_issued = 0, w_used = 0;  // bulk W loads issued / consumed (buffer = index & 1)
-        int j = 0;
-        for (uint32_t i = blockIdx.x; i < nitems; i += gridDim.x) {
-            const Item it = item_of(A, step, i, tshift);
-            if (!it.p) continue;
-            const int b = j++ % NBUF;
-            if (((j - 1) & 1) != wg) continue;
-            const PassDesc P = *it.p;
-            const int slot = it.slot;
-            const uint64_t base = tile_base(P, it.tile);
+        // items of this CTA in order (ordinal jj): raw index blockIdx.x + jj gridDim.x;
+        // warpgroup w processes the ordinals jj = w (mod 2)
+        auto raw = [&](int jj) { return blockIdx.x + (uint32_t)jj * gridDim.x; };
+        // context preparation for ordinal jj into c, by the prep warp: stage A loads the
+        // pass descriptors (registers), stage B stores them, computes the tile bases and
+        // starts the gate-descriptor copies (cp.async group, waited for at the item start)
+        uint4 pd_reg = make_uint4(0, 0, 0, 0);
+        auto prep_a = [&](int jj) {
+            const uint32_t i = raw(jj), i3 = raw(jj + NBUF);
+            if (lane < 4 && i < nitems)
+                pd_reg = reinterpret_cast<const uint4*>(A.step_passes + (i >> tshift))[lane];
+            else if (lane >= 4 && lane < 8 && i3 < nitems)
+                pd_reg = reinterpret_cast<const uint4*>(A.step_passes + (i3 >> tshift))[lane - 4];
+        };
+        auto prep_b = [&](int jj, Ctx* c) {
+            const uint32_t i = raw(jj), i3 = raw(jj + NBUF);
+            if (i >= nitems) return;
+            if (lane < 4) reinterpret_cast<uint4*>(&c->p)[lane] = pd_reg;
+            else if (lane < 8 && i3 < nitems) reinterpret_cast<uint4*>(&c->p3)[lane - 4] = pd_reg;
+            __syncwarp();
+            if (lane == 0) c->base = tile_base(c->p, i & ((1u << tshift) - 1u));
+            if (lane == 1 && i3 < nitems) c->base3 = tile_base(c->p3, i3 & ((1u << tshift) - 1u));
+            const uint4* src = reinterpret_cast<const uint4*>(A.gates + c->p.gate_begin);
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(c->g);
+            const int nch = c->p.gate_count * (int)(sizeof(GateDesc) / 16);
+            for (int k = lane; k < nch; k += 32) cp_async16_s(dst + 16u * (uint32_t)k, src + k);
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+        };
+        // prologue: the first item's context, then the first loads (ordinals 0 and 2 by
+        // warpgroup 0, ordinal 1 by warpgroup 1)
+        if (prep_warp) {
+            prep_a(wg);
+            prep_b(wg, &ctxs[0]);
+        }
+        for (int jj = 0; jj < NBUF; ++jj) {
+            const uint32_t i = raw(jj);
+            if (i < nitems && (jj & 1) == wg) {
+                const Item it = item_of(A, i, tshift);
+                load_item(jj, *it.p, it.tile, tile_base(*it.p, it.tile), wtid);
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+#ifdef QT_V2_TIMING
+        long long t_prev = clock64();
+#define QT_T(k)                                                                              \
+    if (wtid == 0 && blockIdx.x == 7) {                                                      \
+        const long long t_now = clock64();                                                   \
+        atomicAdd(A.timing + (k), (unsigned long long)(t_now - t_prev));                     \
+        t_prev = t_now;                                                                      \
+    }
+#else
+#define QT_T(k)
+#endif
+        int kk = 0;  // this warpgroup's item count
+        for (int jj = wg; raw(jj) < nitems; jj += 2, ++kk) {
+            const uint32_t i = raw(jj);
+            const uint32_t i3 = raw(jj + NBUF);  // loaded into b by this warpgroup when done
+            const int b = jj % NBUF;
+            Ctx* cx = &ctxs[kk & 1];
+            if (prep_warp) asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // this item's gate descriptors
+            bar_wg(wg);  // context visible; the previous item's readers of the other context are done
+            if (prep_warp) prep_a(jj + 2);
+            bool prep_pending = prep_warp;
+            const PassDesc& P = cx->p;
+            const GateDesc* gds = cx->g;
+            const int slot = P.slot;
+            const uint32_t tile_idx = i & ((1u << tshift) - 1u);
             float2* st = A.state + ((uint64_t)slot << n);
             float2* tile = reinterpret_cast<float2*>(sm + (size_t)b * kTileBytes);
             char* const tb8 = reinterpret_cast<char*>(tile);
-            const GateDesc* gates = A.gates + P.gate_begin;
             const int ng = P.gate_count;
-            // W of the first tensor-core gate travels with the tile
+            // W (bulk copies, two buffers): the first two tensor-core gates' operands travel
+            // with the tile; later ones are issued as soon as a buffer's MMAs complete
             int w_next = 0;  // next gate whose W has not been issued
-            while (w_next < ng && !(gates[w_next].k & kGateTC)) ++w_next;
-            if (elect && w_next < ng) {
-                bulk_w(wbuf + (w_issued & 1u) * kV2GateBytes, A.pool + gates[w_next].mat_off,
-                       wfull_bar(wg, (int)(w_issued & 1u)));
-                ++w_issued;
-                ++w_next;
-            }
-            mbar_wait_s(full_bar(b), (uint32_t)((j - 1) / NBUF & 1));
-            float run_scale = 1.f, run_inv = 1.f;
+            // (every thread copies 16 bytes with cp.async; 1-D bulk copies were measured an
+            // order of magnitude slower, profiles/r2_ubench_stream.txt)
+            auto issue_w = [&]() {
+                while (w_next < ng && !(gds[w_next].k & kGateTC)) ++w_next;
+                if (w_next < ng) {
+                    const uint32_t wi = w_issued & 1u;
+                    cp_async16_s(wbuf + wi * kV2GateBytes + 16u * (uint32_t)wtid,
+                                 reinterpret_cast<const char*>(A.pool + gds[w_next].mat_off) + 16 * wtid);
+                    cp_async_arrive_noinc(wfull_bar(wg, (int)wi));
+                    ++w_issued;
+                    ++w_next;
+                }
+            };
+            issue_w();
+            issue_w();
+            const uint64_t base = cx->base, base3 = cx->base3;
+            // one thread polls the tile's mbarrier; the others sleep in the barrier
+            if (elect) mbar_wait_s(full_bar(b), (uint32_t)((jj / NBUF) & 1));
+            bar_wg(wg);
+            QT_T(0);
+            float run_inv = 1.f;
             for (int g = 0; g < ng;) {
-                GateDesc G = gates[g];
-                if (!(G.k & kGateTC)) {
-                    // device-chosen conventional operator (k <= 3) on FP32 CUDA cores, 64 amplitudes per thread
-                    uint32_t unit[6];
+                if (!(gds[g].k & kGateTC)) {
+                    // device-chosen conventional operator (k <= 3) on FP32 CUDA cores, 32 amplitudes per thread
+                    const GateDesc& G = gds[g];
+                    uint32_t unit[5];
 #pragma unroll
-                    for (int m = 0; m < 6; ++m) unit[m] = swz(1u << ((G.rpos >> (4 * m)) & 15u)) << 3;
+                    for (int m = 0; m < 5; ++m) unit[m] = swz(1u << ((G.rpos >> (4 * m)) & 15u)) << 3;
                     uint32_t tb = 0;
 #pragma unroll
-                    for (int q = 0; q < 7; ++q) tb |= ((uint32_t)(wtid >> q) & 1u) << ((G.tpos >> (4 * q)) & 15u);
+                    for (int q = 0; q < 8; ++q) tb |= ((uint32_t)(wtid >> q) & 1u) << ((G.tpos >> (4 * q)) & 15u);
                     const float2* M = A.pool + G.mat_off;
                     const int k = G.k & 0xff;
-                    if (k == 1) apply_fused<1, 6>(tile, M, swz(tb) << 3, unit);
-                    else if (k == 2) apply_fused<2, 6>(tile, M, swz(tb) << 3, unit);
-                    else apply_fused<3, 6>(tile, M, swz(tb) << 3, unit);
+                    if (k == 1) apply_fused<1, 5>(tile, M, swz(tb) << 3, unit);
+                    else if (k == 2) apply_fused<2, 5>(tile, M, swz(tb) << 3, unit);
+                    else apply_fused<3, 5>(tile, M, swz(tb) << 3, unit);
                     bar_wg(wg);
                     ++g;
                     continue;
                 }
                 // ---- segment start: gather the fp32 tile into A (TMEM), new tile scale ----
                 {
-                    uint32_t ucfg[4], ugrp[2], tb = 0;
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) ucfg[m] = swz(1u << ((G.rpos >> (4 * m)) & 15u)) << 3;
-#pragma unroll
-                    for (int a = 0; a < 2; ++a) ugrp[a] = swz(1u << ((G.rpos >> (16 + 4 * a)) & 15u)) << 3;
-#pragma unroll
-                    for (int q = 0; q < 7; ++q) tb |= ((uint32_t)(wtid >> q) & 1u) << ((G.tpos >> (4 * q)) & 15u);
-                    const uint32_t rbase = swz(tb) << 3;
-                    float2 v[64];
+                    const Fp32Layout L = fp32_layout(gds[g], wtid);
+                    uint64_t v[32];
                     float amax = 0.f;
 #pragma unroll
-                    for (int jg = 0; jg < 4; ++jg)
+                    for (int jj = 0; jj < 2; ++jj)
 #pragma unroll
                         for (int c = 0; c < 16; ++c) {
-                            uint32_t o = rbase;
-                            if (jg & 1) o ^= ugrp[0];
-                            if (jg & 2) o ^= ugrp[1];
-#pragma unroll
-                            for (int m = 0; m < 4; ++m)
-                                if ((c >> m) & 1) o ^= ucfg[m];
-                            v[16 * jg + c] = *reinterpret_cast<const float2*>(tb8 + o);
-                            amax = fmaxf(amax, fmaxf(fabsf(v[16 * jg + c].x), fabsf(v[16 * jg + c].y)));
+                            const uint32_t o = (jj ? L.base1 : L.base0) ^ L.c01[c & 3] ^ L.c23[c >> 2];
+                            const float2 f = *reinterpret_cast<const float2*>(tb8 + o);
+                            v[16 * jj + c] = pk2(f.x, f.y);
+                            amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
                         }
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
                     float* redf = reinterpret_cast<float*>(red);
-                    if (lane == 0) redf[warp & 3] = amax;
+                    if (lane == 0) redf[wtid >> 5] = amax;
                     bar_wg(wg);
-                    amax = fmaxf(fmaxf(redf[0], redf[1]), fmaxf(redf[2], redf[3]));
-                    const int shift = (G.k >> kGateShiftBit) & 0xff;
+                    amax = redf[0];
+#pragma unroll
+                    for (int w = 1; w < NWW; ++w) amax = fmaxf(amax, redf[w]);
+                    const int shift = (gds[g].k >> kGateShiftBit) & 0xff;
                     int se = 260 - (int)((__float_as_uint(amax) >> 23) & 0xffu) - shift;  // amax 2^(se-127) in [2^6, 2^7)
                     se = min(max(se, 1), 253);
-                    run_scale = __uint_as_float((uint32_t)se << 23);
+                    const float run_scale = __uint_as_float((uint32_t)se << 23);
                     run_inv = __uint_as_float((uint32_t)(254 - se) << 23);
+                    const uint64_t sc2 = pk2(run_scale, run_scale);
 #pragma unroll
-                    for (int jg = 0; jg < 4; ++jg) {
+                    for (int jj = 0; jj < 2; ++jj) {
                         uint32_t a[32];
 #pragma unroll
-                        for (int c = 0; c < 16; ++c)
-                            split(v[16 * jg + c].x * run_scale, v[16 * jg + c].y * run_scale, a[c], a[16 + c]);
-                        tc::tmem_st32(tl + 64u * (uint32_t)jg + 32u, a);
+                        for (int c = 0; c < 16; ++c) split(mul2(v[16 * jj + c], sc2), a[c], a[16 + c]);
+                        tc::tmem_st32(tlh + 64u * (uint32_t)jj + 32u, a);
                     }
                     tc::tmem_wait_st();
                     tc::fence_before();
                     bar_wg(wg);  // A complete; every fp32 read of this buffer done
+                    QT_T(1);
                 }
                 // ---- the segment's gates ----
                 for (;;) {
-                    if (elect) {
-                        // W(g) (issued earlier, in order), then the MMAs of all four groups
+                    if (issuer) {
+                        // W(g) (issued earlier, in order), then this issuer's group: four issuing
+                        // threads (lane 0 of warps 0..3) keep the tensor pipe fed
                         const uint32_t wi = w_used & 1u;
                         mbar_wait_s(wfull_bar(wg, (int)wi), (w_used >> 1) & 1u);
-                        ++w_used;
+                        tc::fence_proxy_async();  // cp.async (generic proxy) writes -> tensor-core reads
                         tc::fence_after();
                         const uint32_t wb = wbuf + wi * kV2GateBytes;
                         const uint64_t b0 = tc::smem_desc_sw128(wb), b1 = tc::smem_desc_sw128(wb + 32);
                         const uint64_t b2 = tc::smem_desc_sw128(wb + 64), b3 = tc::smem_desc_sw128(wb + 96);
-#pragma unroll
-                        for (int jg = 0; jg < 4; ++jg) {
-                            const uint32_t d = tbase + 64u * (uint32_t)jg, ah = d + 32u, al = d + 48u;
-                            mma_ts(d, ah, b0, 0u);
-                            mma_ts(d, ah + 8u, b1, 1u);
-                            mma_ts(d, al, b0, 1u);
-                            mma_ts(d, al + 8u, b1, 1u);
-                            mma_ts(d, ah, b2, 1u);
-                            mma_ts(d, ah + 8u, b3, 1u);
-                        }
+                        const uint32_t d = tbase + 64u * (uint32_t)(wtid >> 5), ah = d + 32u, al = d + 48u;
+                        mma_ts(d, ah, b0, 0u);
+                        mma_ts(d, ah + 8u, b1, 1u);
+                        mma_ts(d, al, b0, 1u);
+                        mma_ts(d, al + 8u, b1, 1u);
+                        mma_ts(d, ah, b2, 1u);
+                        mma_ts(d, ah + 8u, b3, 1u);
                         tc::mma_commit(reinterpret_cast<uint64_t*>(sm + kMbarOff + 8 * (6 + wg)));
-                        // prefetch the next tensor-core gate's W into the other buffer (its
-                        // previous user, gate g - 1, has completed)
-                        while (w_next < ng && !(gates[w_next].k & kGateTC)) ++w_next;
-                        if (w_next < ng && w_issued == w_used) {
-                            bulk_w(wbuf + (w_issued & 1u) * kV2GateBytes, A.pool + gates[w_next].mat_off,
-                                   wfull_bar(wg, (int)(w_issued & 1u)));
-                            ++w_issued;
-                            ++w_next;
-                        }
+                        QT_T(7);
                     }
+                    ++w_used;
+                    const int32_t gk = gds[g].k;
                     __syncwarp();
-                    mbar_wait_s(mma_bar(wg), mma_phase);
+                    if (prep_pending) {  // in the shadow of the MMAs
+                        prep_b(jj + 2, &ctxs[(kk + 1) & 1]);
+                        prep_pending = false;
+                    }
+                    if (elect) mbar_wait_s(mma_bar(wg), mma_phase);
+                    tc::fence_before();
+                    bar_wg(wg);
+                    QT_T(2);
                     mma_phase ^= 1u;
                     tc::fence_after();
-                    if (G.k & kGateRunEnd) {
+                    issue_w();  // gate g's W buffer is free: the operand of the gate after next
+                    if (gk & kGateRunEnd) {
                         // ---- segment end: D -> fp32 tile ----
-                        uint32_t ucfg[4], ugrp[2], tb = 0;
+                        const Fp32Layout L = fp32_layout(gds[g], wtid);
+                        const uint64_t inv2 = pk2(run_inv, run_inv);
 #pragma unroll
-                        for (int m = 0; m < 4; ++m) ucfg[m] = swz(1u << ((G.rpos >> (4 * m)) & 15u)) << 3;
-#pragma unroll
-                        for (int a = 0; a < 2; ++a) ugrp[a] = swz(1u << ((G.rpos >> (16 + 4 * a)) & 15u)) << 3;
-#pragma unroll
-                        for (int q = 0; q < 7; ++q) tb |= ((uint32_t)(wtid >> q) & 1u) << ((G.tpos >> (4 * q)) & 15u);
-                        const uint32_t rbase = swz(tb) << 3;
-#pragma unroll
-                        for (int jg = 0; jg < 4; ++jg) {
+                        for (int jj = 0; jj < 2; ++jj) {
                             uint32_t d[32];
-                            tc::tmem_ld32(tl + 64u * (uint32_t)jg, d);
+                            tc::tmem_ld32(tlh + 64u * (uint32_t)jj, d);
                             tc::tmem_wait_ld();
-                            uint32_t o0 = rbase;
-                            if (jg & 1) o0 ^= ugrp[0];
-                            if (jg & 2) o0 ^= ugrp[1];
+                            const uint32_t o0 = jj ? L.base1 : L.base0;
 #pragma unroll
                             for (int c = 0; c < 16; ++c) {
-                                uint32_t o = o0;
-#pragma unroll
-                                for (int m = 0; m < 4; ++m)
-                                    if ((c >> m) & 1) o ^= ucfg[m];
-                                *reinterpret_cast<float2*>(tb8 + o) =
-                                    make_float2(__uint_as_float(d[2 * c]) * run_inv, __uint_as_float(d[2 * c + 1]) * run_inv);
+                                const uint32_t o = o0 ^ L.c01[c & 3] ^ L.c23[c >> 2];
+                                *reinterpret_cast<float2*>(tb8 + o) = upk2(
+                                    mul2(pk2(__uint_as_float(d[2 * c]), __uint_as_float(d[2 * c + 1])), inv2));
                             }
                         }
                         tc::fence_before();
                         bar_wg(wg);
+                        QT_T(3);
                         ++g;
                         break;
                     }
                     // ---- in-TMEM transition to gate g + 1: its A from this gate's D ----
-                    {
-                        const uint4 x0 = *reinterpret_cast<const uint4*>(&gates[g].xu[0]);
-                        const uint32_t xu[6] = {x0.x & 0xffffu, x0.x >> 16, x0.y & 0xffffu,
-                                                x0.y >> 16,     x0.z & 0xffffu, x0.z >> 16};
-#pragma unroll 1
-                        for (int jg = 0; jg < 4; ++jg) {
-                            uint32_t cj = tl;
-                            if (jg & 1) cj += xu[4];
-                            if (jg & 2) cj += xu[5];
+                    if (gk & kGateXNext) {
+                        // X: 16x256b loads transpose lanes and columns (profiles/r2_tmem_shapes.txt):
+                        // thread t receives config bits 0, 1 = t & 3 and lane bits 0..2 = t >> 2 of
+                        // this gate, plus lane bit 3 as the register pair; the next gate's rows are
+                        // (config 0, config 1, lane 0, lane 1, lane 2), its matrix bit 0 is lane bit 3
+                        const uint16_t* gu = v2_units(gds[g]) + 14;
+                        uint32_t xv[5];
+#pragma unroll
+                        for (int r = 0; r < 5; ++r) xv[r] = (gu[r] & 0x8000u) ? (16u << 16) : (uint32_t)gu[r];
+                        const uint32_t x01[4] = {0u, xv[0], xv[1], xv[0] + xv[1]};
+#pragma unroll
+                        for (int jj = 0; jj < 2; ++jj) {
+                            const uint32_t ab = tl + (half ? xv[4] : 0u) + (jj ? xv[3] : 0u);
                             uint32_t d[32];
 #pragma unroll
-                            for (int c = 0; c < 16; ++c) {
-                                uint32_t col = cj;
-#pragma unroll
-                                for (int m = 0; m < 4; ++m)
-                                    if ((c >> m) & 1) col += xu[m];
-                                tmem_ld2(col, d[2 * c], d[2 * c + 1]);
+                            for (int q = 0; q < 8; ++q) {
+                                uint32_t r4[4];
+                                tmem_ld_16x256(ab + x01[q & 3] + ((q & 4) ? xv[2] : 0u), r4);
+                                d[4 * q] = r4[0];
+                                d[4 * q + 1] = r4[1];
+                                d[4 * q + 2] = r4[2];
+                                d[4 * q + 3] = r4[3];
                             }
                             tc::tmem_wait_ld();
                             uint32_t a[32];
 #pragma unroll
                             for (int c = 0; c < 16; ++c)
-                                split(__uint_as_float(d[2 * c]), __uint_as_float(d[2 * c + 1]), a[c], a[16 + c]);
-                            tc::tmem_st32(tl + 64u * (uint32_t)jg + 32u, a);
+                                split(pk2(__uint_as_float(d[2 * c]), __uint_as_float(d[2 * c + 1])), a[c], a[16 + c]);
+                            tc::tmem_st32(tlh + 64u * (uint32_t)jj + 32u, a);
+                        }
+                        tc::tmem_wait_st();
+                        tc::fence_before();
+                        bar_wg(wg);
+                    } else {
+                        const uint16_t* gu = v2_units(gds[g]) + 13;
+                        const uint32_t xu[6] = {gu[0], gu[1], gu[2], gu[3], gu[4], gu[5]};
+                        const uint32_t t01[4] = {0u, xu[0], xu[1], xu[0] + xu[1]};
+                        const uint32_t t23[4] = {0u, xu[2], xu[3], xu[2] + xu[3]};
+#pragma unroll
+                        for (int jj = 0; jj < 2; ++jj) {
+                            // output group 2 half + jj
+                            uint32_t cj = tl;
+                            if (half) cj += xu[5];
+                            if (jj) cj += xu[4];
+                            uint32_t d[32];
+#pragma unroll
+                            for (int c = 0; c < 16; ++c) {
+                                tmem_ld2(cj + t01[c & 3] + t23[c >> 2], d[2 * c], d[2 * c + 1]);
+                            }
+                            tc::tmem_wait_ld();
+                            uint32_t a[32];
+#pragma unroll
+                            for (int c = 0; c < 16; ++c) split(pk2(__uint_as_float(d[2 * c]), __uint_as_float(d[2 * c + 1])), a[c], a[16 + c]);
+                            tc::tmem_st32(tlh + 64u * (uint32_t)jj + 32u, a);
                         }
                         tc::tmem_wait_st();
                         tc::fence_before();
                         bar_wg(wg);
                     }
+                    QT_T(8);
                     ++g;
-                    G = gates[g];
                 }
             }
+            if (prep_pending) {
+                prep_b(jj + 2, &ctxs[(kk + 1) & 1]);
+                prep_pending = false;
+            }
             // ---------------- epilogues (read-only on the fp32 tile) ----------------
-            const uint64_t tile_row = (uint64_t)slot * ntiles + it.tile;
+            const uint64_t tile_row = (uint64_t)slot * ntiles + tile_idx;
             if (P.flags & kPassRho) {
                 const EventDesc E = A.events[P.event];
                 const ChanDesc C = A.chans[E.chan];
@@ -515,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                     // last tile of the slot: sum the tile partials in a fixed order, then choose
                     __threadfence();
                     const int ne = 2 * C.d * C.d;
-                    double fin[128];  // ne <= 128 (q <= 3)
+                    double* fin = red + 128;  // ne <= 128 doubles: red[128..255] of this warpgroup
                     const double* part = A.rho_part + (uint64_t)slot * ntiles * A.rho_stride;
                     for (int e0 = 0; e0 < ne; e0 += 8) {
                         double acc[8];
@@ -566,11 +733,13 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                         }
                 for (int o = 0; o < P.obs_count; ++o) {
                     const ObsDesc O = A.obs[P.obs_begin + o];
-                    const uint32_t zl = to_local<T>(O.zmask, P);
+                    // tile-local Z bits (the final pass's tile is the low 13 qubits: a mask)
+                    const uint32_t zl = P.tile_mask == (uint64_t)(TILE - 1) ? (uint32_t)(O.zmask & (TILE - 1))
+                                                                             : to_local<T>(O.zmask, P);
                     const int zs = __popcll(base & O.zmask) & 1;
                     double part[1];
                     if (O.xmask == 0) {
-                        const float vv = pick_uniform<NA>(w, (int)(zl >> 7));
+                        const float vv = pick_uniform<NA>(w, (int)(zl >> 8));
                         const int par = (__popc((uint32_t)wtid & zl & (uint32_t)(NT - 1)) + zs) & 1;
                         part[0] = par ? -(double)vv : (double)vv;
                     } else {
@@ -600,35 +769,53 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                             part[0] += par ? -t : t;
                         }
                     }
-                    wg_sum_n<1>(part, red, wg);
-                    if (wtid == 0) A.obs_part[tile_row * A.n_obs + O.slot] = part[0];
+                    // warp sums parked per (observable, warp); one barrier pair per 16 strings,
+                    // then a fixed-order sum over the 8 warps
+#pragma unroll
+                    for (int sh = 16; sh > 0; sh >>= 1) part[0] += __shfl_xor_sync(0xffffffffu, part[0], sh);
+                    double* park = red + 128;  // 16 strings x 8 warps
+                    const int jo = o & 15;
+                    if (lane == 0) park[jo * NWW + (wtid >> 5)] = part[0];
+                    if (jo == 15 || o + 1 == P.obs_count) {
+                        bar_wg(wg);
+                        if (wtid <= jo) {
+                            double v = 0.0;
+#pragma unroll
+                            for (int w = 0; w < NWW; ++w) v += park[wtid * NWW + w];
+                            A.obs_part[tile_row * A.n_obs + A.obs[P.obs_begin + o - jo + wtid].slot] = v;
+                        }
+                        bar_wg(wg);
+                    }
                 }
             }
             // ---------------- shared -> HBM: 16-byte stores of amplitude pairs ----------------
+            QT_T(4);
             if (P.flags & kPassStore) {
-                // thread: pair p = wtid & 7 of run h = (wtid >> 3) + 16 m
+                // thread: pair p = wtid & 7 of run h = (wtid >> 3) + 32 m
                 const int p = wtid & 7;
                 const uint32_t hl = (uint32_t)(wtid >> 3);
                 uint64_t ofix = 0;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) ofix |= (uint64_t)((hl >> q) & 1u) << P.tq[4 + q];
-                uint64_t M = 0;
+                for (int q = 0; q < 5; ++q) ofix |= (uint64_t)((hl >> q) & 1u) << P.tq[4 + q];
+                float2* dst = st + base + ofix + 2 * p;
+                float2* d1 = dst + (1ull << P.tq[9]);
+                const uint64_t e1 = 1ull << P.tq[10], e2 = 1ull << P.tq[11], e3 = 1ull << P.tq[12];
 #pragma unroll
-                for (int q = 8; q < T; ++q) M |= 1ull << P.tq[q];
-                float4* dst = reinterpret_cast<float4*>(st + base + ofix + 2 * p);
-                uint64_t x = 0;
-#pragma unroll 4
-                for (uint32_t m = 0; m < 32; ++m) {
-                    const uint32_t L = 16u * (hl + 16u * m);
+                for (uint32_t m = 0; m < 16; ++m) {
+                    const uint32_t L = 16u * (hl + 32u * m);
                     const uint32_t s2 = (L ^ ((((L >> 4) ^ (L >> 7) ^ (L >> 10)) & 7u) << 1)) ^ (2u * (uint32_t)p);
                     const float4 v = *reinterpret_cast<const float4*>(tb8 + 8u * s2);
-                    *reinterpret_cast<float4*>(reinterpret_cast<float2*>(dst) + x) = v;
-                    x = (x - M) & M;
+                    const uint64_t x = ((m & 2) ? e1 : 0ull) + ((m & 4) ? e2 : 0ull) + ((m & 8) ? e3 : 0ull);
+                    *reinterpret_cast<float4*>(((m & 1) ? d1 : dst) + x) = v;
                 }
             }
-            bar_wg(wg);  // every read of the buffer done
-            if (elect) mbar_arrive_s(empty_bar(b));
+            bar_wg(wg);  // every read of the buffer and of the staged descriptors done
+            QT_T(5);
+            if (i3 < nitems) load_item(jj + NBUF, cx->p3, i3 & ((1u << tshift) - 1u), base3, wtid);
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+            QT_T(6);
         }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
     }
     tc::fence_before();
     __syncthreads();
@@ -638,6 +825,14 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
 }  // namespace v2
 
 size_t tile_pass_v2_smem_bytes() { return v2::kSmemBytes; }
+#ifdef QT_V2_TIMING
+static unsigned long long* g_v2_tbuf = nullptr;
+// diagnostics build: clock64 phase sums of warpgroup leaders of CTA 7 (16 counters)
+extern "C" void qt_v2_timing_read(unsigned long long* out) {
+    cudaDeviceSynchronize();
+    if (g_v2_tbuf) cudaMemcpy(out, g_v2_tbuf, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+}
+#endif
 
 cudaError_t launch_tile_pass_v2(const TileArgs& a, int step, uint32_t ntiles, int nslots, cudaStream_t s) {
     static bool configured = false;
@@ -656,7 +851,17 @@ cudaError_t launch_tile_pass_v2(const TileArgs& a, int step, uint32_t ntiles, in
     const uint32_t nitems = ntiles * (uint32_t)nslots;
     if (nitems == 0) return cudaSuccess;
     const uint32_t grid = nitems < (uint32_t)sms ? nitems : (uint32_t)sms;
+#ifdef QT_V2_TIMING
+    if (!g_v2_tbuf) {
+        cudaMalloc(&g_v2_tbuf, 16 * sizeof(unsigned long long));
+        cudaMemset(g_v2_tbuf, 0, 16 * sizeof(unsigned long long));
+    }
+    TileArgs b2 = a;
+    b2.timing = g_v2_tbuf;
+    v2::tile_pass_v2_kernel<<<grid, v2::kThreads, v2::kSmemBytes, s>>>(b2, step, nitems, tshift);
+#else
     v2::tile_pass_v2_kernel<<<grid, v2::kThreads, v2::kSmemBytes, s>>>(a, step, nitems, tshift);
+#endif
     return cudaGetLastError();
 }
 

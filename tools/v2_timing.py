@@ -1,0 +1,22 @@
+"""Phase timing of the persistent v2 K1 (-DQT_V2_TIMING build, libqtraj_v2t.so):
+clock64 sums of the warpgroup leaders of CTA 7, per item.
+usage: python tools/v2_timing.py SCRIPT [args]   (runs SCRIPT with the timing library)"""
+import ctypes
+import os
+import runpy
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2111_02396_b200 import qtraj  # noqa: E402
+
+qtraj.LIB_PATH = qtraj.LIB_PATH.replace("libqtraj.so", "libqtraj_v2t.so")
+sys.argv = [sys.argv[1]] + sys.argv[2:]
+runpy.run_path(sys.argv[0], run_name="__main__")
+buf = (ctypes.c_ulonglong * 16)()
+qtraj.lib().qt_v2_timing_read(buf)
+names = ["item start -> tile ready (desc, bases, full wait)", "gather", "MMA complete wait", "write back",
+         "epilogues", "stores + end barrier", "next loads", "W wait + MMA issue", "L/X transition"]
+tot = sum(buf[i] for i in range(9))
+for i, nm in enumerate(names):
+    print(f"  {nm:50s} {buf[i]:14d} cyc  {100.0 * buf[i] / max(tot, 1):5.1f}%")
