@@ -162,7 +162,9 @@ void qt_plan_destroy(qt_plan p);
  * mode: 0 = delayed inner product (Alg. 2).  1 = the conventional
  *   trajectory algorithm the paper compares against: no lower bounds,
  *   every channel is a barrier whose p_i are computed on the device (same
- *   draws, same literal subtract loop with pbar_i = 0); channels of <= 2 qubits. */
+ *   draws, same literal subtract loop with pbar_i = 0).  Channels of up to 6 qubits
+ *   in both modes: conventional channels of 4..6 qubits run on the CUDA-core kernel
+ *   (a tensor-core plan switches to it for such a call; P:203-212 holds for any q). */
 typedef struct {
     uint64_t seed;
     uint64_t traj_begin;
@@ -215,7 +217,7 @@ qt_status qt_expectation_value(qt_ctx ctx, const void* state_dev, int n, int n_o
  * qt_apply_plan: apply every operation of a gate-only plan to a caller state
  *   (2^n amplitudes, in place); QT_EINVAL if the plan holds channels.
  * qt_reduce_rho: rho_Q[a][b] = sum_rest psi[rest,a] conj(psi[rest,b]) over the
- *   local qubits qubits[0..nq) (nq <= 2), fp64, fixed summation order; out =
+ *   local qubits qubits[0..nq) (nq <= 6), fp64, fixed summation order; out =
  *   2 * 4^nq doubles, row-major interleaved, index bit m <-> m-th lowest qubit.
  * qt_sample_local: the chain-rule levels n-1..0 of shots shot_ids[0..nshots)
  *   of a register of n_total qubits whose high bits were already sampled (RNG

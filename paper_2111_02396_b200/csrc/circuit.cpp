@@ -153,6 +153,24 @@ double lower_bound(int d, const cd* K) {
 
 using namespace qt;
 
+namespace qt {
+// Switch a plan to the FP32 CUDA-core kernel (no tensor cores): T = 12 tiles for n >= 12,
+// registers wide enough for every operation and fused gate.
+void cuda_core_plan(Plan& P) {
+    int max_arity = 1;
+    for (const PlanOp& op : P.ops) max_arity = std::max(max_arity, op.nq);
+    P.tc = false;
+    P.v2 = false;
+    if (P.T == 13) P.T = 12;
+    if (P.T >= 12) {
+        P.R = std::max(P.f <= 4 ? 4 : P.f, max_arity);
+    } else {
+        P.R = std::min(P.T, std::max(4, std::max(max_arity, P.f)));
+    }
+    P.f = std::min(P.f, P.R);
+}
+}  // namespace qt
+
 extern "C" {
 
 const char* qt_last_error(void) { return g_last_error.c_str(); }
@@ -531,10 +549,6 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
             po.mixture = mixture;
             if (!mixture) P.max_conv_d = std::max(P.max_conv_d, d);
             P.max_chan_d = std::max(P.max_chan_d, d);
-            if (!mixture && hop->nq > 3) {
-                delete hp;
-                return fail(QT_EARITY, "non-unitary-mixture channels on more than 3 qubits are not supported by the device choose step");
-            }
             // variants: deferred application of K_i (mixtures: K_i / sqrt(pbar_i), exactly unitary)
             for (int i = 0; i < hop->n_kraus; ++i) {
                 const cd* K = hop->mats.data() + (size_t)i * d * d;
@@ -611,6 +625,15 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
         }
         P.ops.push_back(std::move(po));
     }
+    // non-mixture channels on 4..6 qubits: their device-chosen operators (2^q amplitudes
+    // per thread) and rho_Q partials run in the CUDA-core kernel
+    if (P.tc && P.max_conv_d > 8) {
+        if (o.tensor_cores > 0) {
+            delete hp;
+            return fail(QT_EINVAL, "tensor_cores: non-mixture channels on more than 3 qubits need the CUDA-core path");
+        }
+        cuda_core_plan(P);
+    }
     // the f16 tensor-core operands hold matrix entries below 65504: matrices of
     // huge norm (only possible through qt_add_matrix) use the CUDA-core path
     if (P.tc)
@@ -620,11 +643,7 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
                     delete hp;
                     return fail(QT_EINVAL, "tensor_cores: a matrix of norm > 1e3 does not fit the f16 operands");
                 }
-                P.tc = false;
-                P.v2 = false;
-                if (P.T == 13) P.T = 12;  // the CUDA-core kernel tiles 12 qubits
-                P.R = std::max(f <= 4 ? 4 : f, max_arity);
-                P.f = std::min(f, P.R);
+                cuda_core_plan(P);
                 break;
             }
     P.n_channels = chan;

@@ -84,6 +84,9 @@ struct Plan {
     bool has_p00 = false, has_p11 = false;
 };
 
+// Switch a plan to the FP32 CUDA-core kernel (4..6-qubit conventional channels, huge norms).
+void cuda_core_plan(Plan& P);
+
 // Kraus lower bound sigma_min(K)^2 of a d x d matrix.
 double lower_bound(int d, const cd* K);
 

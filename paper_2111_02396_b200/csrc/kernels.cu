@@ -395,6 +395,74 @@ rho_reduce_kernel(const float2* __restrict__ state, int n, uint64_t qmask, int q
     }
 }
 
+// rho_Q of 3..6 qubits (D = 2^q up to 64): block b owns the fixed range of "rest"
+// indices [b R / B, (b + 1) R / B), stages 32 rows of D amplitudes in shared memory
+// and every thread accumulates whole entries (a, b) in a fixed order.
+__global__ void __launch_bounds__(256)
+rho_reduce_big_kernel(const float2* __restrict__ state, int n, uint64_t qmask, int q, double* __restrict__ partial,
+                      int stride) {
+    extern __shared__ float2 xs[];  // [32][D]
+    const int D = 1 << q;
+    const uint64_t rows = 1ull << (n - q);
+    const uint64_t r0 = rows * blockIdx.x / gridDim.x, r1 = rows * (blockIdx.x + 1) / gridDim.x;
+    int qp[6];
+    {
+        uint64_t m = qmask;
+        for (int j = 0; j < q; ++j) {
+            qp[j] = __ffsll((long long)m) - 1;
+            m &= m - 1;
+        }
+    }
+    double acc[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) acc[k] = 0.0;
+    for (uint64_t rc = r0; rc < r1; rc += 32) {
+        const int nr = (int)((r1 - rc) < 32 ? (r1 - rc) : 32);
+        for (int idx = threadIdx.x; idx < nr * D; idx += 256) {
+            const int r = idx / D, a = idx % D;
+            uint64_t g = rc + (uint64_t)r;  // insert the channel bits (ascending positions)
+            for (int j = 0; j < q; ++j) {
+                const uint64_t low = g & ((1ull << qp[j]) - 1ull);
+                g = low | ((g ^ low) << 1) | ((uint64_t)((a >> j) & 1) << qp[j]);
+            }
+            xs[idx] = state[g];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const int e = threadIdx.x + 256 * k;
+            if (e < D * D) {
+                const int a = e / D, b = e % D;
+                double re = acc[2 * k], im = acc[2 * k + 1];
+                for (int r = 0; r < nr; ++r) {
+                    const float2 va = xs[r * D + a], vb = xs[r * D + b];
+                    re += (double)va.x * vb.x + (double)va.y * vb.y;
+                    im += (double)va.y * vb.x - (double)va.x * vb.y;
+                }
+                acc[2 * k] = re;
+                acc[2 * k + 1] = im;
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int e = threadIdx.x + 256 * k;
+        if (e < D * D) {
+            partial[(size_t)blockIdx.x * stride + 2 * e] = acc[2 * k];
+            partial[(size_t)blockIdx.x * stride + 2 * e + 1] = acc[2 * k + 1];
+        }
+    }
+}
+
+__global__ void rho_final_big_kernel(const double* __restrict__ partial, int ne, int stride, double* __restrict__ out) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int b = 0; b < kRhoBlocks; ++b) s += partial[(size_t)b * stride + e];
+        out[e] = s;
+    }
+}
+
 __global__ void rho_final_kernel(const double* __restrict__ partial, int ne, double* __restrict__ out) {
     const int e = threadIdx.x;
     if (e >= ne) return;
@@ -445,6 +513,14 @@ cudaError_t launch_permute_qubits(const float2* src, float2* dst, int n, const i
 
 cudaError_t launch_rho_reduce(const float2* state, int n, uint64_t qmask, int q, double* partial, double* out,
                               cudaStream_t s) {
+    if (q >= 3) {
+        const int D = 1 << q, stride = 2 * D * D;
+        rho_reduce_big_kernel<<<kRhoBlocks, 256, sizeof(float2) * 32 * D, s>>>(state, n, qmask, q, partial, stride);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        rho_final_big_kernel<<<(stride + 255) / 256, 256, 0, s>>>(partial, stride, stride, out);
+        return cudaGetLastError();
+    }
     rho_reduce_kernel<<<kRhoBlocks, 256, 0, s>>>(state, n, qmask, q, partial);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -64,8 +64,8 @@ cudaError_t launch_sample(const float2* state, int n, int T, const double* block
 // dst[pi(i)] = src[i] where bit b of i moves to bit perm[b] (n <= 24).
 cudaError_t launch_permute_qubits(const float2* src, float2* dst, int n, const int* perm, cudaStream_t s);
 
-// rho_Q (2^q x 2^q, q <= 2) of the qubits in qmask over a whole n-qubit state;
-// partial: kRhoBlocks x 32 doubles scratch; out: 2 * 4^q doubles (device).
+// rho_Q (2^q x 2^q, q <= 6) of the qubits in qmask over a whole n-qubit state;
+// partial: 296 x max(32, 2 * 4^q) doubles scratch; out: 2 * 4^q doubles (device).
 cudaError_t launch_rho_reduce(const float2* state, int n, uint64_t qmask, int q, double* partial, double* out,
                               cudaStream_t s);
 

@@ -373,7 +373,7 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
     QT_CK(B.pool.ensure(sizeof(float2) * std::max<int32_t>(pool, 2)));
     QT_CK(B.status.ensure(sizeof(int32_t) * nslots));
     QT_CK(B.counters.ensure(sizeof(int32_t) * nslots));
-    const int rd = std::min(P.max_chan_d, 8);  // conventional mode reduces every channel (q <= 3)
+    const int rd = P.max_chan_d;  // conventional mode reduces every channel (q <= 6)
     const int rho_stride = 2 * rd * rd;
     QT_CK(B.rho_part.ensure(sizeof(double) * (size_t)nslots * ntiles * rho_stride));
     QT_CK(B.blocksum.ensure(sizeof(double) * (size_t)nslots * ntiles));
@@ -588,10 +588,17 @@ qt_status qt_run_trajectories(qt_ctx ctx, qt_plan plan, const qt_run_opts* opts,
     if (!ctx || !plan || !opts || !state_dev) return fail(QT_EINVAL, "NULL argument");
     if (n_obs < 0 || (n_obs > 0 && !obs)) return fail(QT_EINVAL, "bad observables");
     if (opts->mode != 0 && opts->mode != 1) return fail(QT_EINVAL, "mode must be 0 (delayed) or 1 (conventional)");
-    if (opts->mode == 1 && plan_of(plan).max_chan_d > 8)
-        return fail(QT_EARITY, "conventional mode reduces every channel: channels on more than 3 qubits are not supported");
     if (opts->shots_per_traj < 0) return fail(QT_EINVAL, "shots_per_traj < 0");
-    const Plan& P = plan_of(plan);
+    // conventional mode reduces every channel: channels on 4..6 qubits need the
+    // CUDA-core kernel (its device-chosen operators hold 2^6 amplitudes per thread)
+    Plan fallback;
+    const Plan* Pp = &plan_of(plan);
+    if (opts->mode == 1 && Pp->max_chan_d > 8 && Pp->tc) {
+        fallback = *Pp;
+        cuda_core_plan(fallback);
+        Pp = &fallback;
+    }
+    const Plan& P = *Pp;
     QT_CK(cudaSetDevice(ctx->device));
     const size_t per = sizeof(float2) << P.n;
     const size_t max_slots = state_bytes / per;
@@ -934,7 +941,7 @@ qt_status qt_apply_plan(qt_ctx ctx, qt_plan plan, void* state_dev, size_t state_
 
 qt_status qt_reduce_rho(qt_ctx ctx, const void* state_dev, int n, int nq, const int* qubits, double* out) {
     if (!ctx || !state_dev || !qubits || !out) return fail(QT_EINVAL, "NULL argument");
-    if (nq < 1 || nq > 2) return fail(QT_EARITY, "qt_reduce_rho: 1 or 2 qubits");
+    if (nq < 1 || nq > 6) return fail(QT_EARITY, "qt_reduce_rho: 1..6 qubits");
     uint64_t qmask = 0;
     for (int i = 0; i < nq; ++i) {
         if (qubits[i] < 0 || qubits[i] >= n) return fail(QT_EQUBIT, "qubit out of range");
@@ -944,9 +951,10 @@ qt_status qt_reduce_rho(qt_ctx ctx, const void* state_dev, int n, int nq, const 
     QT_CK(cudaSetDevice(ctx->device));
     BatchBufs& B = ctx->bb[0];
     if (finish_batch(B, Plan(), 0, 0, CallOut{}) != QT_OK) return QT_ECUDA;
-    QT_CK(B.rho_part.ensure(sizeof(double) * 296 * 32 + sizeof(double) * 32));
+    const size_t stride = std::max<size_t>(32, (size_t)2 << (2 * nq));
+    QT_CK(B.rho_part.ensure(sizeof(double) * (296 * stride + stride)));
     double* partial = B.rho_part.as<double>();
-    double* dout = partial + 296 * 32;
+    double* dout = partial + 296 * stride;
     QT_CK(launch_rho_reduce(reinterpret_cast<const float2*>(state_dev), n, qmask, nq, partial, dout, ctx->stream));
     QT_CK(cudaMemcpyAsync(out, dout, sizeof(double) * (2 << (2 * nq)), cudaMemcpyDeviceToHost, ctx->stream));
     QT_CK(cudaStreamSynchronize(ctx->stream));

@@ -327,6 +327,46 @@ __device__ __forceinline__ void rho_partial_rows(const float2* tile, uint32_t ql
     }
 }
 
+// rho_Q partial of a Q = 4..6 qubit channel (D = 2^Q up to 64): every thread owns
+// whole entries (a, b) of the D x D matrix and sums them over the tile's 2^(T - Q)
+// rows in a fixed order, so no block reduction is needed; entries are written
+// straight to `out` (2 D^2 doubles, re / im interleaved, row-major).  A rare path
+// (non-mixture channels on many qubits): slow, shared-memory reads only.
+template <int T, int NT, typename Swz>
+__device__ __forceinline__ void rho_partial_big(const float2* tile, uint32_t qlocal, int nq, double* out, Swz swzf) {
+    const int D = 1 << nq;
+    const uint32_t rows = 1u << (T - nq);
+    const uint32_t rest = ((1u << T) - 1u) & ~qlocal;
+    for (int e = threadIdx.x; e < D * D; e += NT) {
+        const int a = e / D, b = e % D;
+        const uint32_t oa = pdep32((uint32_t)a, qlocal), ob = pdep32((uint32_t)b, qlocal);
+        double re = 0.0, im = 0.0;
+        for (uint32_t r = 0; r < rows; ++r) {
+            const uint32_t bL = pdep32(r, rest);
+            const float2 va = tile[swzf(bL | oa)], vb = tile[swzf(bL | ob)];
+            // rho[a][b] += psi[a] conj(psi[b])
+            re += (double)va.x * vb.x + (double)va.y * vb.y;
+            im += (double)va.y * vb.x - (double)va.x * vb.y;
+        }
+        out[2 * e] = re;
+        out[2 * e + 1] = im;
+    }
+}
+
+// Last tile of a slot, Q >= 4: entry-parallel fixed-order sums of the tile partials,
+// written over tile 0's partial (each entry read before it is overwritten by the
+// same thread); returns the final rho_Q (global memory).
+template <int NT>
+__device__ __forceinline__ const double* rho_final_big(double* part, uint32_t ntiles, int stride, int ne) {
+    for (int e = threadIdx.x; e < ne; e += NT) {
+        double s = 0.0;
+        for (uint32_t t = 0; t < ntiles; ++t) s += __ldcg(part + (uint64_t)t * stride + e);
+        part[e] = s;
+    }
+    __threadfence_block();
+    return part;
+}
+
 // Alg. 2 lines 13-21 for one conventional channel, single thread.
 static __device__ __noinline__ void choose_conventional(const EventDesc& E, const ChanDesc& C, const double* cd,
                                     const double* rho /*2*d*d*/, float2* pool, int32_t* records,

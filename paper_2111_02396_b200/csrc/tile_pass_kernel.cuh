@@ -798,7 +798,9 @@ tile_pass_kernel(const TileArgs A, const int step) {
         const ChanDesc C = A.chans[E.chan];
         const uint32_t ql = to_local<T>(C.qmask, P);  // channel qubits as tile-local bits
         double* out = A.rho_part + tile_row * A.rho_stride;
-        if constexpr (T >= 3) {
+        if (C.nq >= 4) {
+            rho_partial_big<T, NT>(tile, ql, C.nq, out, [](uint32_t L) { return swz(L); });
+        } else if constexpr (T >= 3) {
             if (C.nq == 1) rho_partial<1, T, NT>(tile, ql, out, red);
             else if (C.nq == 2) rho_partial<2, T, NT>(tile, ql, out, red);
             else rho_partial_rows<3, T, NT>(tile, ql, out, red);
@@ -817,8 +819,17 @@ tile_pass_kernel(const TileArgs A, const int step) {
             // strided over threads, then a fixed-order block sum), 8 entries at a time
             __threadfence();
             const int ne = 2 * C.d * C.d;
-            double* fin = reinterpret_cast<double*>(gdesc);  // ne <= 32 doubles (gate descriptors are done)
+            double* fin = reinterpret_cast<double*>(gdesc);  // ne <= 128 doubles (gate descriptors are done)
             const double* part = A.rho_part + (uint64_t)slot * ntiles * A.rho_stride;
+            if (C.nq >= 4) {  // 4..6 qubits: entry-parallel sums in global memory
+                const double* rf = rho_final_big<NT>(A.rho_part + (uint64_t)slot * ntiles * A.rho_stride, ntiles,
+                                                     A.rho_stride, ne);
+                __syncthreads();
+                if (tid == 0) {
+                    choose_conventional(E, C, A.chan_data, rf, A.pool, A.records, A.status + slot);
+                    A.counters[slot] = 0;
+                }
+            } else
             for (int e0 = 0; e0 < ne; e0 += 8) {
                 double acc[8];
 #pragma unroll
@@ -833,10 +844,12 @@ tile_pass_kernel(const TileArgs A, const int step) {
                     for (int j = 0; j < 8; ++j)
                         if (e0 + j < ne) fin[e0 + j] = acc[j];
             }
-            __syncthreads();
-            if (tid == 0) {
-                choose_conventional(E, C, A.chan_data, fin, A.pool, A.records, A.status + slot);
-                A.counters[slot] = 0;
+            if (C.nq < 4) {
+                __syncthreads();
+                if (tid == 0) {
+                    choose_conventional(E, C, A.chan_data, fin, A.pool, A.records, A.status + slot);
+                    A.counters[slot] = 0;
+                }
             }
         }
     }

@@ -155,3 +155,56 @@ def test_three_qubit_conventional_channels(ctx, n, mode):
     ref, out, state = run_both(ctx, c, seed=23, T=16, shots=2, mode=mode)
     assert (ref["branch"] == 1).any()
     assert compare(ref, out, state) == 0
+
+
+def parity_projectors(q):
+    """{P_even, P_odd} on q qubits (parity of the computational-basis bits): a
+    projective (s = 0, always conventional) q-qubit channel."""
+    d = 2 ** q
+    par = np.array([bin(i).count("1") & 1 for i in range(d)])
+    return [np.diag((par == 0).astype(float)).astype(np.complex128), np.diag((par == 1).astype(float)).astype(np.complex128)]
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("n", [9, 13])
+def test_four_to_six_qubit_conventional_channels(ctx, n, mode):
+    """Alg. 2 lines 13-21 for channels on 4 and 6 qubits (P:203-212 hold for any q):
+    a 4-qubit product of amplitude damping (16 Kraus operators of 16 x 16, non-mixture)
+    and a 6-qubit parity-projective channel (s = 0); rho_Q up to 64 x 64 on the device.
+    Both modes; the conventional mode also reduces a 4-qubit depolarizing mixture."""
+    rng = np.random.default_rng(n + 100 * mode)
+    a1, a2 = channels.amplitude_damp(0.3), channels.amplitude_damp(0.15)
+    ad4 = [np.kron(np.kron(np.kron(a, b), c), d) for a in a1 for b in a2 for c in a1 for d in a2]
+    proj6 = parity_projectors(6)
+    dep1 = channels.depolarize(0.04)
+    moms = []
+    for layer in range(3):
+        moms.append([Gate((q,), workloads.haar_unitary(rng, 2)) for q in range(n)])
+        moms.append([Gate((0, n - 1), workloads.haar_unitary(rng, 4)), Gate((2, 3), workloads.haar_unitary(rng, 4))])
+        moms.append([Channel((1, n - 2, 4, 5), ad4)])
+        moms.append([Channel(tuple(range(n - 6, n))[::-1], proj6), Channel((0,), dep1)])
+    c = Circuit(n_qubits=n, moments=moms, observables=["Z" * n, "X" + "I" * (n - 2) + "Z"])
+    ref, out, state = run_both(ctx, c, seed=29, T=12, shots=2, mode=mode)
+    assert (ref["branch"] == 1).any()
+    assert compare(ref, out, state) == 0
+
+
+@pytest.mark.parametrize("nq", [1, 2, 3, 4, 5, 6])
+def test_reduce_rho_up_to_six_qubits(ctx, nq):
+    """qt_reduce_rho (distributed-state building block) for 1..6 qubits vs numpy:
+    rho_Q[a][b] = sum_rest psi[rest, a] conj(psi[rest, b]), index bit m <-> m-th
+    lowest listed qubit."""
+    n = 14
+    rng = np.random.default_rng(nq)
+    psi = rng.standard_normal(2 ** n) + 1j * rng.standard_normal(2 ** n)
+    psi = (psi / np.linalg.norm(psi)).astype(np.complex64)
+    qs = sorted(int(x) for x in rng.choice(n, size=nq, replace=False))
+    st = torch.from_numpy(psi).cuda()
+    rho = ctx.reduce_rho(st, qs)
+    t = psi.astype(np.complex128).reshape([2] * n)  # axis i <-> qubit n-1-i
+    axes = [n - 1 - q for q in qs]
+    rest = [a for a in range(n) if a not in axes]
+    # matrix index bit m <-> qubits[m] (ascending): the most significant index bit is qs[-1]
+    tt = np.transpose(t, rest + axes[::-1]).reshape(-1, 2 ** nq)
+    want = tt.T @ tt.conj()
+    assert np.allclose(rho, want, atol=1e-6), np.abs(rho - want).max()

@@ -108,3 +108,26 @@ def test_noisy_circuit_is_valid_and_runs():
     assert n_decay == c.n_qubits * len(c.moments)
     r = oracle.run_trajectories(noisy, seed=2, traj_count=20)
     assert r["rc"] == 0 and np.all(r["status"] == 0)
+
+
+def test_coherent_error_z_phases_before_and_after_P424():
+    """P:424 puts the Z phase errors before AND after the fSim gate.  The inserted error
+    unitary E (applied after the ideal gate G) must give E G = Z_a fSim(th + dth, ph + dph)
+    Z_b, checked through the fSim composition law on a gate that does not commute with
+    Z x I (sqrt-iSWAP-like fSim(pi/4, 0)), with different phases on the two qubits."""
+    th0, ph0 = np.pi / 4, 0.0
+    G = workloads.gates.fsim(th0, ph0)
+    pc = nm.PairCal(0.01, d_theta=0.03, d_phi=-0.02, z_before=(0.05, -0.04), z_after=(0.02, 0.07))
+    M = nm.QCSNoiseModel(qubits={0: nm.QubitCal(1e4, 1e-3, 1e-3), 1: nm.QubitCal(1e4, 1e-3, 1e-3)},
+                         pairs={(0, 1): pc})
+    E = M.coherent_2q((0, 1), G)
+    ez = lambda a: np.diag([np.exp(1j * a), np.exp(-1j * a)])  # e^{i a Z} (P:424)
+    zb = np.kron(ez(0.05), ez(-0.04))
+    za = np.kron(ez(0.02), ez(0.07))
+    want = za @ workloads.gates.fsim(th0 + 0.03, ph0 - 0.02) @ zb
+    got = E @ G
+    k = np.vdot(want.ravel(), got.ravel())
+    assert abs(abs(k) - 4) < 1e-9, k  # equal up to a global phase
+    assert np.allclose(got, want * (k / abs(k)), atol=1e-12)
+    # the phases do not commute through G: the old placement (all after G) differs
+    assert not np.allclose(M.coherent_2q((0, 1)) @ G, got, atol=1e-6)

@@ -125,19 +125,25 @@ class QCSNoiseModel:
     def r_inc(self, q: int, t: float) -> float:
         return pauli_error(self.decay(q, t))
 
-    def coherent_2q(self, pair: Tuple[int, int]) -> np.ndarray:
-        """Z phases before, fSim(d_theta, d_phi), Z phases after (Kronecker order of pair)."""
+    def coherent_2q(self, pair: Tuple[int, int], G: Optional[np.ndarray] = None) -> np.ndarray:
+        """The coherent error E inserted AFTER the ideal gate G of the pair, so that
+        E G = Z_after fSim(d_theta, d_phi) G Z_before: Z phase errors before and after
+        the gate and the fSim angle deviations (fSim gates compose
+        additively).  E = Z_after fSim(d) G Z_before G^dagger (Kronecker order of pair);
+        G = None means identity (no Z_before / G reordering)."""
         pc = self.pairs.get(pair, PairCal(0.0))
         zb = np.kron(z_phase(pc.z_before[0]), z_phase(pc.z_before[1]))
         za = np.kron(z_phase(pc.z_after[0]), z_phase(pc.z_after[1]))
-        return za @ gates.fsim(pc.d_theta, pc.d_phi) @ zb
+        if G is None:
+            return za @ gates.fsim(pc.d_theta, pc.d_phi) @ zb
+        return za @ gates.fsim(pc.d_theta, pc.d_phi) @ G @ zb @ G.conj().T
 
-    def r_ent(self, pair: Tuple[int, int]) -> float:
-        return pauli_error([self.coherent_2q(pair)])
+    def r_ent(self, pair: Tuple[int, int], G: Optional[np.ndarray] = None) -> float:
+        return pauli_error([self.coherent_2q(pair, G)])
 
-    def r_dep_2q(self, pair: Tuple[int, int]) -> float:
+    def r_dep_2q(self, pair: Tuple[int, int], G: Optional[np.ndarray] = None) -> float:
         pc = self.pairs.get(pair, PairCal(0.0))
-        r = pc.xeb_pauli - self.r_inc(pair[0], self.t_2q) - self.r_inc(pair[1], self.t_2q) - self.r_ent(pair)
+        r = pc.xeb_pauli - self.r_inc(pair[0], self.t_2q) - self.r_inc(pair[1], self.t_2q) - self.r_ent(pair, G)
         return max(0.0, r)
 
     def r_dep_1q(self, q: int) -> float:
@@ -157,8 +163,8 @@ class QCSNoiseModel:
                     continue
                 qs = tuple(op.qubits)
                 if len(qs) == 2:
-                    coherent.append(Gate(qs, self.coherent_2q(qs), "coherent_err"))
-                    r = self.r_dep_2q(qs)
+                    coherent.append(Gate(qs, self.coherent_2q(qs, op.matrix), "coherent_err"))
+                    r = self.r_dep_2q(qs, op.matrix)
                     if r > 0:
                         depol.append(Channel(qs, channels.depolarize2(r), "depolarize2"))
                 elif len(qs) == 1:
