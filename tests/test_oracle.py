@@ -47,17 +47,66 @@ def test_philox_known_answers():
         assert oracle.philox(v[0:4], v[4:6]) == v[6:10]
 
 
+def _golden_rng():
+    """Parse tests/golden/rng_contract.txt (written by tools/gen_rng_golden.py, a third
+    Philox implementation): list of (purpose, traj, shot, [(ordinal, half)], values)."""
+    path = os.path.join(os.path.dirname(__file__), "golden", "rng_contract.txt")
+    rows, n = [], 4
+    half_n = (n + 1) // 2
+    for ln in open(path):
+        if ln.startswith("#") or "->" not in ln:
+            continue
+        head, vals = ln.split("->")
+        vals = vals.split()
+        f = head.split()
+        kv = dict(x.split("=") for x in f if "=" in x)
+        if f[0] == "channel":
+            t = int(kv["traj"])
+            if "ordinals" in f:
+                rows.append((oracle.PURPOSE_CHANNEL, t, [(c, 0) for c in range(3)], [float(v) for v in vals]))
+            else:
+                rows.append((oracle.PURPOSE_CHANNEL, t, [(int(f[-1]), 0)], [float(v) for v in vals]))
+        elif f[0] == "sample":
+            t, sh = int(kv["traj"]), int(kv["shot"])
+            rows.append((oracle.PURPOSE_SAMPLE, t, [(sh * half_n + l // 2, l % 2) for l in (3, 2, 1, 0)],
+                         [float(v) for v in vals]))
+        elif f[0] == "readout":
+            t, sh = int(kv["traj"]), int(kv["shot"])
+            rows.append((oracle.PURPOSE_READOUT, t, [(sh * half_n + q // 2, q % 2) for q in range(4)],
+                         [float(v) for v in vals]))
+    return rows
+
+
 def test_rng_contract_golden():
+    """Oracle draws = the golden vectors of an independent third Philox (CHANNEL,
+    SAMPLE at shots 0..3, READOUT ordinals shot * ceil(n/2) + q/2, a trajectory index
+    above 2^32), plus the Random123-style block of (ordinal 0, CHANNEL)."""
     seed = 0x23962112
     assert oracle.philox([0, 1, 0, 0], [seed, 0]) == [0x861C02A8, 0xB8423366, 0x81CEF5B7, 0x5D2ED471]
-    exp0 = [0.52386490791857343, 0.35796686453032722, 0.5727855321855464]
-    exp1 = [0.7985919120810705, 0.31354188185699172, 0.16664808336856729]
-    for i in range(3):
-        assert oracle.uniform(seed, i, oracle.PURPOSE_CHANNEL, 0) == exp0[i]
-        assert oracle.uniform(seed, i, oracle.PURPOSE_CHANNEL, 1) == exp1[i]
-    exps = [0.95160282898675452, 0.57369501685412683, 0.51156285187175676, 0.074121588276452099]
-    for l, e in zip((3, 2, 1, 0), exps):
-        assert oracle.uniform(seed, l // 2, oracle.PURPOSE_SAMPLE, 0, l % 2) == e
+    rows = _golden_rng()
+    assert len(rows) >= 9
+    for purpose, t, ords, vals in rows:
+        for (o, h), v in zip(ords, vals):
+            assert oracle.uniform(seed, o, purpose, t, h) == v, (purpose, t, o, h)
+
+
+def test_rng_golden_generator_reproduces_file():
+    """The committed golden file is exactly what tools/gen_rng_golden.py writes."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "gen_rng_golden.py"), "--check"])
+    assert r.returncode == 0
+
+
+def test_library_host_rng_matches_golden():
+    """The product's own Philox (csrc/philox.hpp, host side of libqtraj, qt_draw) gives
+    the same golden draws (the device copy is the same header; parity tests cover it)."""
+    from paper_2111_02396_b200 import qtraj
+    seed = 0x23962112
+    for purpose, t, ords, vals in _golden_rng():
+        for (o, h), v in zip(ords, vals):
+            assert qtraj.draw(seed, o, purpose, t, h) == v
 
 
 def test_u53_range_and_resolution():
@@ -217,6 +266,30 @@ def test_ghz4_density_matrix_closed_forms():
     assert abs(sum(probs[1:15]) - 0.0392950835) < 1e-9
 
 
+def test_density_matrix_readout_path_closed_form_and_trajectories():
+    """dm.outcome_probabilities with readout error (reading R14): on |1>|0>
+    the recorded distribution is the product of the two confusion rows in closed
+    form; on a noisy 3-qubit circuit the oracle's trajectory bitstrings (readout
+    applied) follow it (chi-square)."""
+    rho = np.zeros((4, 4)); rho[1, 1] = 1.0  # qubit 0 = 1, qubit 1 = 0
+    p00, p11 = np.array([0.1, 0.2]), np.array([0.3, 0.05])
+    probs = dm.outcome_probabilities(rho, p00, p11)
+    # qubit 0 (|1>): recorded 0 with p11[0]; qubit 1 (|0>): recorded 1 with p00[1]
+    want = {1: (1 - 0.3) * (1 - 0.2), 0: 0.3 * (1 - 0.2), 3: (1 - 0.3) * 0.2, 2: 0.3 * 0.2}
+    for x, w in want.items():
+        assert abs(probs[x] - w) < 1e-15
+    c = workloads.random_circuit(3, depth=4, seed=9, noise="both", p=0.05, t1_ns=900.0, tphi_ns=1500.0,
+                                 readout=True)
+    rho = dm.evolve(c)
+    pr = dm.outcome_probabilities(rho, c.p00, c.p11)
+    R = 40000
+    r = oracle.run_trajectories(c, seed=5, traj_count=R, shots=1)
+    hist = np.bincount(r["bits"][:, 0].astype(np.int64), minlength=8)
+    m = pr > 0
+    chi2 = (((hist[m] - R * pr[m]) ** 2) / (R * pr[m])).sum()
+    assert chi2 < 7 + 6 * np.sqrt(14)
+
+
 def test_ghz4_trajectories_golden_histogram_and_stats():
     c = workloads.ghz4_depolarized(0.01)
     seed = workloads.trajectory_seed(1)
@@ -338,6 +411,78 @@ def test_sampler_distribution_chi_square():
     # unnormalized input gives the same samples (norm invariance)
     bits2, _ = oracle.sample_state(psi * 3.0, seed=4, traj=3, shots=1000)
     assert (bits2 == bits[:1000]).all()
+
+
+def _chain_rule_bruteforce(psi, seed, traj, shot, draw):
+    """Reading R13 written out by enumeration (independent of oracle.c): masses of the
+    two children of the current prefix summed over ALL 2^n probabilities that carry
+    the prefix, one fresh uniform per level (SAMPLE ordinal shot * ceil(n/2) + l // 2,
+    half l % 2, from the third Philox of tools/gen_rng_golden.py)."""
+    n = int(np.log2(psi.size))
+    p = np.abs(np.asarray(psi, np.complex128)) ** 2
+    idx = np.arange(psi.size)
+    half_n = (n + 1) // 2
+    prefix = 0
+    for l in range(n - 1, -1, -1):
+        hi = ((idx >> (l + 1)) << (l + 1)) == prefix  # indices with the chosen bits above l
+        m0 = p[hi & (((idx >> l) & 1) == 0)].sum()
+        m1 = p[hi & (((idx >> l) & 1) == 1)].sum()
+        u = draw(seed, shot * half_n + l // 2, 2, traj, l % 2)
+        if m0 == 0.0:
+            bit = 1
+        elif m1 == 0.0:
+            bit = 0
+        else:
+            bit = 0 if u * (m0 + m1) < m0 else 1
+        prefix |= bit << l
+    return prefix
+
+
+def test_sampler_chain_rule_bruteforce_enumeration():
+    """Every oracle sample equals the brute-force enumeration of the chain-rule map
+    (n <= 10; Porter-Thomas-like, GHZ-like and basis states, i.e. zero-mass branches),
+    up to decisions whose margin is below 1e-12 (different fp64 summation orders)."""
+    import importlib.util
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("gen_rng_golden", os.path.join(root, "tools", "gen_rng_golden.py"))
+    g = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(g)
+    rng = np.random.default_rng(12)
+    states = []
+    for n in (1, 3, 6, 10):
+        states.append(rand_state(rng, n))
+    ghz = np.zeros(2 ** 7, np.complex128); ghz[0] = ghz[-1] = np.sqrt(0.5)
+    basis = np.zeros(2 ** 5, np.complex128); basis[19] = 1.0
+    sparse = rand_state(rng, 8) * (rng.random(256) < 0.1)
+    states += [ghz, basis, sparse / np.linalg.norm(sparse)]
+    checked = 0
+    for k, psi in enumerate(states):
+        shots = 40
+        bits, margins = oracle.sample_state(psi, seed=0x5EED + k, traj=3 + k, shots=shots)
+        for sh in range(shots):
+            want = _chain_rule_bruteforce(psi, 0x5EED + k, 3 + k, sh, g.draw)
+            if margins[sh] >= 1e-12:
+                assert int(bits[sh]) == want, (k, sh)
+                checked += 1
+    assert checked > 250
+
+
+def test_chain_rule_map_measure_equals_probability():
+    """The chain-rule map sends the uniform measure on [0,1)^n to |psi|^2 exactly:
+    enumerate a 64-point midpoint grid per level on n = 2 and count outcomes."""
+    psi = np.array([0.5, 0.5j, np.sqrt(0.375), -np.sqrt(0.125)], np.complex128)
+    p = np.abs(psi) ** 2
+    G = 64
+    grid = (np.arange(G) + 0.5) / G
+    counts = np.zeros(4)
+    for u1 in grid:          # level 1 (the MSB) first
+        m0, m1 = p[0] + p[1], p[2] + p[3]
+        b1 = 0 if u1 * (m0 + m1) < m0 else 1
+        for u0 in grid:
+            c0, c1 = p[2 * b1], p[2 * b1 + 1]
+            b0 = 0 if u0 * (c0 + c1) < c0 else 1
+            counts[2 * b1 + b0] += 1
+    assert np.allclose(counts / G ** 2, p, atol=1.0 / G)
 
 
 def test_readout_flips():
