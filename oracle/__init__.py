@@ -63,7 +63,7 @@ def lib():
         L.orc_run_trajectories.argtypes = (
             [ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, vp,
              ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64,
-             ctypes.c_int, ctypes.c_int, ctypes.c_int] + [vp] * 9)
+             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int] + [vp] * 9)
         L.orc_run_trajectories.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -134,11 +134,14 @@ class TrajectoryResult(dict):
 
 def run_trajectories(circuit, seed: int, traj_begin: int = 0, traj_count: int = 1,
                      stride: int = 1, shots: int = 1, threads: int = None,
-                     want_states: bool = False, mode: int = 0) -> TrajectoryResult:
+                     want_states: bool = False, mode: int = 0, range_parallel: bool = False) -> TrajectoryResult:
     """Alg. 2 trajectories t = traj_begin + stride*j, j < traj_count.
 
     mode 0 = delayed inner products (Alg. 2); mode 1 = the conventional
     trajectory algorithm (every channel computes its p_i).
+    range_parallel: parallel mode (ii) (for n >= 24): one
+    trajectory at a time, the Alg. 1 outer loop of every pass split into 64 fixed
+    index ranges over `threads` threads; results are identical to mode (i).
     `circuit` is a workloads.Circuit.  Returns numpy arrays keyed by name."""
     from workloads import flatten  # input serialization only
     f = flatten(circuit)
@@ -165,7 +168,8 @@ def run_trajectories(circuit, seed: int, traj_begin: int = 0, traj_count: int = 
         n, n_ops, _ptr(f["kind"]), _ptr(f["nq"]), _ptr(qubits), _ptr(f["n_kraus"]),
         _ptr(f["mat_off"]), _ptr(f["mats"]), _ptr(p00), _ptr(p11), n_obs,
         ctypes.addressof(obs_buf) if obs_buf is not None else None,
-        seed, traj_begin, stride, T, shots, threads, mode,
+        seed, traj_begin, stride, T, shots, 1 if range_parallel else threads, mode,
+        threads if range_parallel else 0,
         _ptr(states), _ptr(out["kraus"]), _ptr(out["branch"]), _ptr(out["kraus_margin"]),
         _ptr(out["bits"]), _ptr(out["bits_raw"]), _ptr(out["sample_margin"]),
         _ptr(out["obs"]), _ptr(out["status"]))

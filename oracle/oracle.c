@@ -38,6 +38,7 @@
  *   R14 readout: a recorded 0 flips to 1 with probability p00[q], a recorded
  *      1 flips to 0 with probability p11[q]; one READOUT draw per (shot,qubit).
  */
+#define _POSIX_C_SOURCE 200809L  /* pthread barriers under -std=c11 */
 #include <complex.h>
 #include <math.h>
 #include <pthread.h>
@@ -53,6 +54,82 @@ typedef double complex cplx;
 #define ORC_ESTATE -10
 
 enum { PURPOSE_CHANNEL = 1, PURPOSE_SAMPLE = 2, PURPOSE_READOUT = 3 };
+
+/* ------------------------------------------------------------------------ */
+/* Fixed index-range decomposition (mode (ii) of BASELINE.md section 3: the  */
+/* Alg. 1 outer loop split into disjoint ranges).  Every loop over    */
+/* the 2^n amplitudes runs as NCHUNK contiguous ranges, and every fp64 sum   */
+/* is the sum of the NCHUNK range sums in range order -- in BOTH modes, so   */
+/* results do not depend on the thread count (reading R11: fp64 reductions, */
+/* order unspecified by the paper).  With a pool, ranges are spread over     */
+/* threads (range r on thread r mod T) and a barrier ends every operation.   */
+/* ------------------------------------------------------------------------ */
+#define NCHUNK 64
+
+typedef struct pool_s {
+    int nthreads; /* including the calling thread */
+    pthread_t th[256];
+    pthread_barrier_t start, done;
+    void (*fn)(void* arg, int chunk);
+    void* arg;
+    int quit;
+} pool_t;
+
+typedef struct { pool_t* P; int tid; } pool_arg_t;
+
+static void* pool_worker(void* a) {
+    pool_arg_t* pa = (pool_arg_t*)a;
+    pool_t* P = pa->P;
+    for (;;) {
+        pthread_barrier_wait(&P->start);
+        if (P->quit) break;
+        for (int c = pa->tid; c < NCHUNK; c += P->nthreads) P->fn(P->arg, c);
+        pthread_barrier_wait(&P->done);
+    }
+    return NULL;
+}
+
+/* run fn(arg, c) for c = 0..NCHUNK-1 (in parallel with a pool, serially without) */
+static void par_for(pool_t* P, void (*fn)(void*, int), void* arg) {
+    if (!P || P->nthreads <= 1) {
+        for (int c = 0; c < NCHUNK; ++c) fn(arg, c);
+        return;
+    }
+    P->fn = fn;
+    P->arg = arg;
+    pthread_barrier_wait(&P->start);
+    for (int c = 0; c < NCHUNK; c += P->nthreads) fn(arg, c);
+    pthread_barrier_wait(&P->done);
+}
+
+static pool_arg_t g_pool_args[256];
+
+static pool_t* pool_create(int nthreads) {
+    if (nthreads <= 1) return NULL;
+    if (nthreads > 64) nthreads = 64;
+    pool_t* P = calloc(1, sizeof(pool_t));
+    P->nthreads = nthreads;
+    pthread_barrier_init(&P->start, NULL, (unsigned)nthreads);
+    pthread_barrier_init(&P->done, NULL, (unsigned)nthreads);
+    for (int t = 1; t < nthreads; ++t) {
+        g_pool_args[t].P = P;
+        g_pool_args[t].tid = t;
+        pthread_create(&P->th[t], NULL, pool_worker, &g_pool_args[t]);
+    }
+    return P;
+}
+
+static void pool_destroy(pool_t* P) {
+    if (!P) return;
+    P->quit = 1;
+    pthread_barrier_wait(&P->start);
+    for (int t = 1; t < P->nthreads; ++t) pthread_join(P->th[t], NULL);
+    pthread_barrier_destroy(&P->start);
+    pthread_barrier_destroy(&P->done);
+    free(P);
+}
+
+static uint64_t chunk_lo(uint64_t dim, int c) { return dim * (uint64_t)c / NCHUNK; }
 
 /* ------------------------------------------------------------------------ */
 /* Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11), written out plainly.   */
@@ -109,23 +186,40 @@ static uint64_t subvector_index(uint64_t base, int nq, const int* qubits,
     return idx;
 }
 
-static void apply_matrix(cplx* psi, int n, int nq, const int* qubits,
-                         const cplx* U) {
-    int M = 1 << nq;
+typedef struct {
+    cplx* psi;
+    int n, nq;
+    const int* qubits;
+    const cplx* U;
+} apply_arg_t;
+
+/* Alg. 1 over the bases of one index range (the subvectors are disjoint) */
+static void apply_chunk(void* a, int c) {
+    const apply_arg_t* A = (const apply_arg_t*)a;
+    int M = 1 << A->nq;
     uint64_t gate_mask = 0;
-    for (int m = 0; m < nq; ++m) gate_mask |= (uint64_t)1 << qubits[m];
+    for (int m = 0; m < A->nq; ++m) gate_mask |= (uint64_t)1 << A->qubits[m];
     cplx v[64], w[64];
-    uint64_t dim = (uint64_t)1 << n;
-    for (uint64_t base = 0; base < dim; ++base) {
+    uint64_t dim = (uint64_t)1 << A->n;
+    for (uint64_t base = chunk_lo(dim, c); base < chunk_lo(dim, c + 1); ++base) {
         if (base & gate_mask) continue; /* one base per subvector */
-        for (int k = 0; k < M; ++k) v[k] = psi[subvector_index(base, nq, qubits, k)];
+        for (int k = 0; k < M; ++k) v[k] = A->psi[subvector_index(base, A->nq, A->qubits, k)];
         for (int j = 0; j < M; ++j) {
             cplx acc = 0;
-            for (int k = 0; k < M; ++k) acc += U[j * M + k] * v[k];
+            for (int k = 0; k < M; ++k) acc += A->U[j * M + k] * v[k];
             w[j] = acc;
         }
-        for (int j = 0; j < M; ++j) psi[subvector_index(base, nq, qubits, j)] = w[j];
+        for (int j = 0; j < M; ++j) A->psi[subvector_index(base, A->nq, A->qubits, j)] = w[j];
     }
+}
+
+static void apply_matrix_p(pool_t* P, cplx* psi, int n, int nq, const int* qubits, const cplx* U) {
+    apply_arg_t A = {psi, n, nq, qubits, U};
+    par_for(P, apply_chunk, &A);
+}
+
+static void apply_matrix(cplx* psi, int n, int nq, const int* qubits, const cplx* U) {
+    apply_matrix_p(NULL, psi, n, nq, qubits, U);
 }
 
 int orc_apply_gate(double* psi_interleaved, int n, int nq, const int* qubits,
@@ -140,16 +234,76 @@ int orc_apply_gate(double* psi_interleaved, int n, int nq, const int* qubits,
     return ORC_OK;
 }
 
-static double norm2(const cplx* psi, int n) {
+typedef struct {
+    cplx* psi;
+    const cplx* src;
+    uint64_t dim;
+    double a;
+    double part[NCHUNK];
+    cplx cpart[NCHUNK];
+} vec_arg_t;
+
+static void norm_chunk(void* p, int c) {
+    vec_arg_t* A = (vec_arg_t*)p;
     double s = 0.0;
-    uint64_t dim = (uint64_t)1 << n;
-    for (uint64_t i = 0; i < dim; ++i) s += creal(psi[i]) * creal(psi[i]) + cimag(psi[i]) * cimag(psi[i]);
-    return s;
+    for (uint64_t i = chunk_lo(A->dim, c); i < chunk_lo(A->dim, c + 1); ++i)
+        s += creal(A->src[i]) * creal(A->src[i]) + cimag(A->src[i]) * cimag(A->src[i]);
+    A->part[c] = s;
 }
 
-static void scale(cplx* psi, int n, double a) {
-    uint64_t dim = (uint64_t)1 << n;
-    for (uint64_t i = 0; i < dim; ++i) psi[i] *= a;
+/* ||psi||^2: range sums, then their sum in range order */
+static double norm2_p(pool_t* P, const cplx* psi, int n) {
+    vec_arg_t A;
+    A.src = psi;
+    A.dim = (uint64_t)1 << n;
+    par_for(P, norm_chunk, &A);
+    double s = 0.0;
+    for (int c = 0; c < NCHUNK; ++c) s += A.part[c];
+    return s;
+}
+static double norm2(const cplx* psi, int n) { return norm2_p(NULL, psi, n); }
+
+static void scale_chunk(void* p, int c) {
+    vec_arg_t* A = (vec_arg_t*)p;
+    for (uint64_t i = chunk_lo(A->dim, c); i < chunk_lo(A->dim, c + 1); ++i) A->psi[i] *= A->a;
+}
+static void scale_p(pool_t* P, cplx* psi, int n, double a) {
+    vec_arg_t A;
+    A.psi = psi;
+    A.dim = (uint64_t)1 << n;
+    A.a = a;
+    par_for(P, scale_chunk, &A);
+}
+
+static void copy_chunk(void* p, int c) {
+    vec_arg_t* A = (vec_arg_t*)p;
+    const uint64_t lo = chunk_lo(A->dim, c), hi = chunk_lo(A->dim, c + 1);
+    memcpy(A->psi + lo, A->src + lo, sizeof(cplx) * (hi - lo));
+}
+static void copy_p(pool_t* P, cplx* dst, const cplx* src, int n) {
+    vec_arg_t A;
+    A.psi = dst;
+    A.src = src;
+    A.dim = (uint64_t)1 << n;
+    par_for(P, copy_chunk, &A);
+}
+
+/* sum_i conj(x_i) y_i: range sums in range order */
+static void dot_chunk(void* p, int c) {
+    vec_arg_t* A = (vec_arg_t*)p;
+    cplx s = 0;
+    for (uint64_t i = chunk_lo(A->dim, c); i < chunk_lo(A->dim, c + 1); ++i) s += conj(A->src[i]) * A->psi[i];
+    A->cpart[c] = s;
+}
+static cplx dot_p(pool_t* P, const cplx* x, cplx* y, int n) {
+    vec_arg_t A;
+    A.src = x;
+    A.psi = y;
+    A.dim = (uint64_t)1 << n;
+    par_for(P, dot_chunk, &A);
+    cplx s = 0;
+    for (int c = 0; c < NCHUNK; ++c) s += A.cpart[c];
+    return s;
 }
 
 /* ------------------------------------------------------------------------ */
@@ -276,7 +430,7 @@ static double min_d(double a, double b) { return a < b ? a : b; }
  * trajectory algorithm of P:181 -- no lower bounds (pbar_i = 0), so every
  * channel computes its p_i = ||K_i psi||^2 and samples with the same literal
  * subtract loop (Alg. 2's second loop with pbar = 0). */
-static int sample_channel(cplx* psi, int n, int nq, const int* qubits, int nk,
+static int sample_channel(pool_t* PL, cplx* psi, int n, int nq, const int* qubits, int nk,
                           const cplx* Ks, double u, int mode, int* chosen, int* branch,
                           double* margin) {
     int d = 1 << nq;
@@ -310,9 +464,9 @@ static int sample_channel(cplx* psi, int n, int nq, const int* qubits, int nk,
         cplx* tmp = malloc(sizeof(cplx) * dim);
         double p[64], w[64];
         for (int i = 0; i < nk; ++i) {
-            memcpy(tmp, psi, sizeof(cplx) * dim);
-            apply_matrix(tmp, n, nq, qubits, Ks + (size_t)i * d * d);
-            p[i] = norm2(tmp, n);
+            copy_p(PL, tmp, psi, n);
+            apply_matrix_p(PL, tmp, n, nq, qubits, Ks + (size_t)i * d * d);
+            p[i] = norm2_p(PL, tmp, n);
             if (p[i] < pbar[i] - 1e-6) { free(tmp); return ORC_EINVAL; }
             w[i] = p[i] - pbar[i];
             if (w[i] < 0.0) w[i] = 0.0;
@@ -329,39 +483,64 @@ static int sample_channel(cplx* psi, int n, int nq, const int* qubits, int nk,
                 if (w[i] > 0.0) { pick = i; break; }
             if (pick < 0) { free(tmp); return ORC_ELEAK; }
         }
-        memcpy(tmp, psi, sizeof(cplx) * dim);
-        apply_matrix(tmp, n, nq, qubits, Ks + (size_t)pick * d * d);
+        copy_p(PL, tmp, psi, n);
+        apply_matrix_p(PL, tmp, n, nq, qubits, Ks + (size_t)pick * d * d);
         /* |Psi> <- (1/sqrt(p_i)) K_i |Psi>  (Alg. 2 line 16) */
-        scale(tmp, n, 1.0 / sqrt(p[pick]));
-        memcpy(psi, tmp, sizeof(cplx) * dim);
+        scale_p(PL, tmp, n, 1.0 / sqrt(p[pick]));
+        copy_p(PL, psi, tmp, n);
         free(tmp);
         *chosen = pick; *branch = 1; *margin = mg;
         return ORC_OK;
     }
 apply_normalized:
-    apply_matrix(psi, n, nq, qubits, Ks + (size_t)(*chosen) * d * d);
+    apply_matrix_p(PL, psi, n, nq, qubits, Ks + (size_t)(*chosen) * d * d);
     {
-        double nn = norm2(psi, n);
+        double nn = norm2_p(PL, psi, n);
         if (!(nn > 0.0)) return ORC_ESTATE;
-        scale(psi, n, 1.0 / sqrt(nn));
+        scale_p(PL, psi, n, 1.0 / sqrt(nn));
     }
     return ORC_OK;
 }
 
-/* Chain-rule sampler (R13): returns the bitstring; margin = min over levels. */
-static uint64_t sample_one(const cplx* psi, int n, uint64_t seed, uint64_t traj,
+/* Chain-rule sampler (R13): returns the bitstring; margin = min over levels.
+ * The masses of the two children of the prefix are range sums (NCHUNK ranges of
+ * the 2^l completions, summed in range order). */
+typedef struct {
+    const cplx* psi;
+    uint64_t prefix;
+    int l;
+    double m0[NCHUNK], m1[NCHUNK];
+} mass_arg_t;
+
+static void mass_chunk(void* p, int c) {
+    mass_arg_t* A = (mass_arg_t*)p;
+    const uint64_t lo_count = (uint64_t)1 << A->l;
+    double M0 = 0.0, M1 = 0.0;
+    for (uint64_t low = chunk_lo(lo_count, c); low < chunk_lo(lo_count, c + 1); ++low) {
+        uint64_t i0 = A->prefix | low;                      /* bit l = 0 */
+        uint64_t i1 = A->prefix | ((uint64_t)1 << A->l) | low; /* bit l = 1 */
+        M0 += creal(A->psi[i0]) * creal(A->psi[i0]) + cimag(A->psi[i0]) * cimag(A->psi[i0]);
+        M1 += creal(A->psi[i1]) * creal(A->psi[i1]) + cimag(A->psi[i1]) * cimag(A->psi[i1]);
+    }
+    A->m0[c] = M0;
+    A->m1[c] = M1;
+}
+
+static uint64_t sample_one(pool_t* PL, const cplx* psi, int n, uint64_t seed, uint64_t traj,
                            int shot, double* margin) {
     uint64_t prefix = 0; /* bits above the current level */
     double mg = INFINITY;
     int half_n = (n + 1) / 2;
+    mass_arg_t A;
+    A.psi = psi;
     for (int l = n - 1; l >= 0; --l) {
+        A.prefix = prefix;
+        A.l = l;
+        par_for(PL, mass_chunk, &A);
         double M0 = 0.0, M1 = 0.0;
-        uint64_t lo_count = (uint64_t)1 << l;
-        for (uint64_t low = 0; low < lo_count; ++low) {
-            uint64_t i0 = prefix | low;                 /* bit l = 0 */
-            uint64_t i1 = prefix | ((uint64_t)1 << l) | low; /* bit l = 1 */
-            M0 += creal(psi[i0]) * creal(psi[i0]) + cimag(psi[i0]) * cimag(psi[i0]);
-            M1 += creal(psi[i1]) * creal(psi[i1]) + cimag(psi[i1]) * cimag(psi[i1]);
+        for (int c = 0; c < NCHUNK; ++c) {
+            M0 += A.m0[c];
+            M1 += A.m1[c];
         }
         double u = orc_uniform(seed, (uint32_t)(shot * half_n + l / 2),
                                PURPOSE_SAMPLE, traj, l % 2);
@@ -397,27 +576,26 @@ static uint64_t readout(uint64_t bits, int n, const double* p00,
 
 /* <psi|P|psi> / <psi|psi> with P = tensor product of single-qubit Paulis,
  * computed by applying each Pauli with Alg. 1 to a copy. */
-static double pauli_expectation(const cplx* psi, int n, const char* ps) {
+static double pauli_expectation(pool_t* PL, const cplx* psi, int n, const char* ps) {
     static const cplx X[4] = {0, 1, 1, 0};
     static const cplx Y[4] = {0, -I, I, 0};
     static const cplx Z[4] = {1, 0, 0, -1};
     uint64_t dim = (uint64_t)1 << n;
     cplx* phi = malloc(sizeof(cplx) * dim);
-    memcpy(phi, psi, sizeof(cplx) * dim);
+    copy_p(PL, phi, psi, n);
     for (int q = 0; q < n; ++q) {
         const cplx* P = NULL;
         if (ps[q] == 'X') P = X;
         else if (ps[q] == 'Y') P = Y;
         else if (ps[q] == 'Z') P = Z;
-        if (P) apply_matrix(phi, n, 1, &q, P);
+        if (P) apply_matrix_p(PL, phi, n, 1, &q, P);
     }
-    cplx num = 0;
-    for (uint64_t i = 0; i < dim; ++i) num += conj(psi[i]) * phi[i];
+    cplx num = dot_p(PL, psi, phi, n);
     free(phi);
-    return creal(num) / norm2(psi, n);
+    return creal(num) / norm2_p(PL, psi, n);
 }
 
-static int run_one(const orc_circuit* c, uint64_t seed, uint64_t traj,
+static int run_one(pool_t* PL, const orc_circuit* c, uint64_t seed, uint64_t traj,
                    int shots, orc_traj_out* o) {
     int n = c->n;
     uint64_t dim = (uint64_t)1 << n;
@@ -430,12 +608,12 @@ static int run_one(const orc_circuit* c, uint64_t seed, uint64_t traj,
     for (int op = 0; op < c->n_ops && status == ORC_OK; ++op) {
         const int* qs = c->qubits + 6 * op;
         if (c->kind[op] == 0) {
-            apply_matrix(psi, n, c->nq[op], qs, mats + c->mat_off[op]);
+            apply_matrix_p(PL, psi, n, c->nq[op], qs, mats + c->mat_off[op]);
         } else {
             double u = orc_uniform(seed, (uint32_t)ch, PURPOSE_CHANNEL, traj, 0);
             int chosen = -1, branch = -1;
             double margin = INFINITY;
-            status = sample_channel(psi, n, c->nq[op], qs, c->n_kraus[op],
+            status = sample_channel(PL, psi, n, c->nq[op], qs, c->n_kraus[op],
                                     mats + c->mat_off[op], u, c->mode, &chosen, &branch,
                                     &margin);
             if (o->kraus_choice) o->kraus_choice[ch] = chosen;
@@ -447,13 +625,13 @@ static int run_one(const orc_circuit* c, uint64_t seed, uint64_t traj,
     if (status == ORC_OK) {
         for (int s = 0; s < shots; ++s) {
             double mg;
-            uint64_t b = sample_one(psi, n, seed, traj, s, &mg);
+            uint64_t b = sample_one(PL, psi, n, seed, traj, s, &mg);
             if (o->bits_raw) o->bits_raw[s] = b;
             if (o->sample_margin) o->sample_margin[s] = mg;
             if (o->bits) o->bits[s] = readout(b, n, c->p00, c->p11, seed, traj, s);
         }
         for (int k = 0; k < c->n_obs; ++k)
-            if (o->obs_values) o->obs_values[k] = pauli_expectation(psi, n, c->obs + (size_t)k * n);
+            if (o->obs_values) o->obs_values[k] = pauli_expectation(PL, psi, n, c->obs + (size_t)k * n);
         if (o->final_state) memcpy(o->final_state, psi, sizeof(cplx) * dim);
     }
     free(psi);
@@ -481,6 +659,7 @@ typedef struct {
     int32_t* status;
     int64_t next;
     pthread_mutex_t lock;
+    pool_t* pool;  /* mode (ii): range-parallel trajectories, one at a time */
 } job_t;
 
 static void* worker(void* arg) {
@@ -500,7 +679,7 @@ static void* worker(void* arg) {
         o.bits_raw = J->bits_raw ? J->bits_raw + (int64_t)J->shots * j : NULL;
         o.sample_margin = J->sample_margin ? J->sample_margin + (int64_t)J->shots * j : NULL;
         o.obs_values = J->obs_values ? J->obs_values + (int64_t)J->c->n_obs * j : NULL;
-        int st = run_one(J->c, J->seed, J->traj_begin + J->stride * (uint64_t)j, J->shots, &o);
+        int st = run_one(J->pool, J->c, J->seed, J->traj_begin + J->stride * (uint64_t)j, J->shots, &o);
         if (J->status) J->status[j] = st;
     }
     return NULL;
@@ -511,11 +690,11 @@ int orc_run_trajectories(
     const int* n_kraus, const int64_t* mat_off, const double* mats,
     const double* p00, const double* p11, int n_obs, const char* obs,
     uint64_t seed, uint64_t traj_begin, uint64_t stride, int64_t traj_count,
-    int shots, int n_threads, int mode,
+    int shots, int n_threads, int mode, int range_threads,
     double* final_states, int32_t* kraus_choice, int8_t* branch,
     double* kraus_margin, uint64_t* bits, uint64_t* bits_raw,
     double* sample_margin, double* obs_values, int32_t* status) {
-    if (n < 1 || n > 30 || n_ops < 0 || shots < 0 || traj_count < 0) return ORC_EINVAL;
+    if (n < 1 || n > 34 || n_ops < 0 || shots < 0 || traj_count < 0) return ORC_EINVAL;
     if (mode != 0 && mode != 1) return ORC_EINVAL;
     orc_circuit c = {n, n_ops, kind, nq, qubits, n_kraus, mat_off, mats,
                      p00, p11, n_obs, obs, mode};
@@ -529,11 +708,19 @@ int orc_run_trajectories(
     J.kraus_margin = kraus_margin; J.bits = bits; J.bits_raw = bits_raw;
     J.sample_margin = sample_margin; J.obs_values = obs_values; J.status = status;
     pthread_mutex_init(&J.lock, NULL);
-    if (n_threads < 1) n_threads = 1;
-    if (n_threads > 256) n_threads = 256;
-    pthread_t th[256];
-    for (int t = 0; t < n_threads; ++t) pthread_create(&th[t], NULL, worker, &J);
-    for (int t = 0; t < n_threads; ++t) pthread_join(th[t], NULL);
+    if (range_threads > 1) {
+        /* mode (ii): one trajectory at a time, every pass range-parallel */
+        J.pool = pool_create(range_threads);
+        worker(&J);
+        pool_destroy(J.pool);
+    } else {
+        /* mode (i): one trajectory per thread */
+        if (n_threads < 1) n_threads = 1;
+        if (n_threads > 256) n_threads = 256;
+        pthread_t th[256];
+        for (int t = 0; t < n_threads; ++t) pthread_create(&th[t], NULL, worker, &J);
+        for (int t = 0; t < n_threads; ++t) pthread_join(th[t], NULL);
+    }
     pthread_mutex_destroy(&J.lock);
     int worst = ORC_OK;
     if (status)
@@ -546,14 +733,14 @@ int orc_run_trajectories(
 int orc_sample_state(const double* psi_interleaved, int n, uint64_t seed,
                      uint64_t traj, int shots, uint64_t* bits, double* margins) {
     for (int s = 0; s < shots; ++s)
-        bits[s] = sample_one((const cplx*)psi_interleaved, n, seed, traj, s,
+        bits[s] = sample_one(NULL, (const cplx*)psi_interleaved, n, seed, traj, s,
                              margins ? &margins[s] : &(double){0});
     return ORC_OK;
 }
 
 double orc_pauli_expectation(const double* psi_interleaved, int n,
                              const char* paulis) {
-    return pauli_expectation((const cplx*)psi_interleaved, n, paulis);
+    return pauli_expectation(NULL, (const cplx*)psi_interleaved, n, paulis);
 }
 
 int orc_is_unitary_mixture(int d, int nk, const double* Ks) {

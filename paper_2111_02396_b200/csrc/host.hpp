@@ -5,6 +5,7 @@
 #include <complex>
 #include <cstdint>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "../../include/qtraj.h"

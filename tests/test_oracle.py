@@ -548,3 +548,19 @@ def test_conventional_mode_kraus_frequencies():
     counts = np.bincount(r["kraus"][:, 0], minlength=4)
     exp = np.array([0.7, 0.1, 0.1, 0.1]) * R
     assert (((counts - exp) ** 2) / exp).sum() < 11.34  # chi-square 3 dof, alpha = 0.01
+
+
+def test_range_parallel_mode_matches_trajectory_parallel_mode():
+    """Oracle parallel mode (ii) (the Alg. 1 outer loop split into
+    fixed index ranges, for n >= 24) gives exactly the results of mode (i): same Kraus
+    choices, margins, samples, observables and states, bit for bit (fixed range-sum
+    order in both modes)."""
+    c = workloads.random_circuit(13, depth=6, seed=21, noise="both", p=0.03, t1_ns=600.0, tphi_ns=900.0,
+                                 readout=True)
+    a = oracle.run_trajectories(c, seed=8, traj_count=3, shots=3, want_states=True, threads=3)
+    b = oracle.run_trajectories(c, seed=8, traj_count=3, shots=3, want_states=True, threads=5,
+                                range_parallel=True)
+    assert a["rc"] == 0 and b["rc"] == 0
+    assert (a["branch"] == 1).any()
+    for k in ("kraus", "branch", "kraus_margin", "bits", "bits_raw", "sample_margin", "obs", "states"):
+        assert np.array_equal(a[k], b[k]), k
