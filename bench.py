@@ -15,6 +15,13 @@ Weak scaling (trajectories are independent units, no data-path
 collective; one all-reduce of observable sums per step): per-GPU work is fixed,
 value = N * 10^4 trajectories / step time (max over ranks).
 
+At N > 1 the line also carries "strong": C2's own split (10^4 trajectories over
+the N GPUs, 10^4 / N per rank).  Extra keys (driver-visible numbers of the other
+BASELINE configs): "c1" (GHZ-4, 1000 trajectories), "c3" (26-qubit low-noise grid at
+f = 4 and f = 6), "c4" (one 32-qubit noisy trajectory) and the gate-pass HBM sweep at
+n = 32 (C4 (i)); "plan" = host planning cost per trajectory (one core) and whether it
+hides behind the device work.
+
 `python bench.py --impl reference` times the CPU oracle (plain fp64 C, one
 trajectory per host core) on the same workload: the reference arm of this tier.
 """
@@ -187,10 +194,56 @@ def gate_pass_sweep(ctx, n, dev, hbm_peak, reps=10):
             "k4_median_frac": float(np.median([r["frac"] for r in rows if r["k"] <= 4])), "rows": rows}
 
 
+def other_configs(ctx, dev, host_threads):
+    """Driver-visible numbers of BASELINE configs 1, 3 and 4 (ii):
+    device-timed trajectories/s of one launch sequence each (inputs resident)."""
+    import torch
+    from paper_2111_02396_b200 import qtraj
+    out = {}
+
+    def timed(circ, f, count, batch, seed, reps=2):
+        c = qtraj.Circuit.from_description(circ)
+        plan = qtraj.Plan(c, max_fused=f)
+        st = torch.empty(batch << circ.n_qubits, dtype=torch.complex64, device=dev)
+        ctx.run_trajectories(plan, st, seed=seed, traj_count=min(count, batch), shots=1, batch=batch,
+                             observables=circ.observables, host_threads=host_threads)  # warm-up
+        best = None
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            o = ctx.run_trajectories(plan, st, seed=seed, traj_count=count, shots=1, batch=batch,
+                                     observables=circ.observables, host_threads=host_threads)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        info = plan.info(seed, 0)
+        s = o["stats"]
+        del st
+        torch.cuda.empty_cache()
+        return {"trajectories": count, "ms": best, "traj_per_s": count / (best / 1e3),
+                "passes_per_traj": s["passes"] / max(count, 1), "fused_gates_per_traj": s["fused_gates"] / max(count, 1),
+                "reductions_per_traj": s["reductions"] / max(count, 1), "tile_bits": int(info["tile_bits"]),
+                "kernel": int(info["kernel"])}
+
+    out["c1"] = dict(workload="C1 GHZ-4 + depolarize(0.01)",
+                     **timed(workloads.ghz4_depolarized(0.01), 4, 1000, 1000, workloads.trajectory_seed(1)))
+    c3 = workloads.low_noise_grid()
+    out["c3"] = {"workload": "C3 26q 2x13 low-noise grid, 20 cycles"}
+    for f in (4, 6):
+        out["c3"][f"f{f}"] = timed(c3, f, 128, 32, workloads.trajectory_seed(3))
+    c4 = workloads.low_noise_grid(rows=4, cols=8, config=4, damping="amplitude")
+    out["c4"] = dict(workload="C4 (ii) one 32q noisy trajectory (4x8 grid, 20 cycles, depolarize + amplitude damping)",
+                     **timed(c4, 4, 1, 1, workloads.trajectory_seed(4), reps=1))
+    return out
+
+
 def bench_gpu(args):
     import torch
     import torch.distributed as dist
-    from paper_2111_02396_b200 import qtraj
+    from paper_2111_02396_b200 import dispatch, qtraj
     rank, world, local = rank_env()
     torch.cuda.set_device(local)
     if world > 1:
@@ -250,7 +303,31 @@ def bench_gpu(args):
     tot_ms = float(t.item())
     value = world * TOTAL_TRAJ * args.steps / (tot_ms / 1e3)
 
-    # ---- e2e: host circuit arrays -> C ABI (upload, fuse, run) -> host results
+    # ---- strong scaling (C2's own split: 10^4 trajectories over the N GPUs)
+    strong = None
+    if world > 1:
+        sb, ss, sc = dispatch.shard(TOTAL_TRAJ, rank, world)
+        s_times = []
+        for _ in range(max(1, min(args.steps, 3))):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctx.run_trajectories(plan, state, seed=seed, traj_count=sc, traj_begin=sb, traj_stride=ss, shots=1,
+                                 batch=batch, observables=obs, host_threads=host_threads)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            s_times.append(e0.elapsed_time(e1))
+        ts = torch.tensor([float(np.mean(s_times))], device=dev, dtype=torch.float64)
+        dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+        strong = {"value": TOTAL_TRAJ / (float(ts.item()) / 1e3), "unit": UNIT, "ms_per_step": float(ts.item()),
+                  "trajectories_per_step": TOTAL_TRAJ, "trajectories_per_gpu": TOTAL_TRAJ // world,
+                  "scaling": "strong"}
+
+    # ---- e2e: host circuit arrays -> C ABI (upload, fuse, run) -> records of every rank
+    # merged through the dispatcher (one all-gather) -> host aggregate (mean, stderr)
     e2e_times = []
     for _ in range(max(1, min(args.steps, 2))):
         flush.fill_(1)
@@ -261,17 +338,28 @@ def bench_gpu(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         c2, plan2 = build_plan(circ, args.fuse)
-        o2 = ctx.run_trajectories(plan2, state, seed=seed, traj_count=count, traj_begin=begin, traj_stride=stride,
-                                  shots=1, batch=batch, observables=obs, host_threads=host_threads)
-        mean = o2["obs"].mean(0)
+
+        def runner(b, s_, n_):
+            return ctx.run_trajectories(plan2, state, seed=seed, traj_count=n_, traj_begin=b, traj_stride=s_,
+                                        shots=1, batch=batch, observables=obs, host_threads=host_threads)
+        merged = dispatch.run_sharded(runner, world * TOTAL_TRAJ, device=dev if world > 1 else None)
+        mean, se = dispatch.aggregate(merged["obs"])
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_times.append(e0.elapsed_time(e1))
-        del c2, plan2, mean
+        del c2, plan2, mean, se, merged
     te = torch.tensor([float(np.mean(e2e_times))], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * TOTAL_TRAJ / (float(te.item()) / 1e3)
+
+    # ---- host planning cost (Alg. 2 first loop + fusion + passes), one core
+    pinfo = plan.info(seed, 0)
+    t0 = time.perf_counter()
+    NPL = 200
+    for j in range(NPL):
+        plan.info(seed, 17 + 50 * j)
+    plan_core_ms = 1e3 * (time.perf_counter() - t0) / NPL
     st0 = stats[-1]
     h2d = circuit_bytes(circ) + st0["h2d_bytes"]  # circuit upload + plan tables + trajectory programs
     d2h = st0["d2h_bytes"]                        # bitstrings, Kraus records, observables, status
@@ -306,30 +394,33 @@ def bench_gpu(args):
                 "fp32_equivalent": {"achieved_tflops": achieved_tf, "peak_tflops": fp32_peak_tf, "frac": frac_alu,
                                      "note": "fused-gate flops (P:135) vs the FP32 pipes; context only: the tensor-core K1 runs them on tcgen05"}}
     # second in-SM resource of the tensor-core K1: every fused gate's epilogue reads its
-    # accumulator D from TMEM, 64 fp32 columns per 16-amplitude row = 16 B per amplitude
-    # (f16 runs: [x W_hi | x_hi W_lo] halves; 3xTF32 gates: two 32-column accumulators);
-    # TMEM read throughput 64 B/cycle/SM (B300_MICROARCH.md "LDTM throughput", same
-    # tcgen05 TMEM on sm_100a) at the sampled SM clock
+    # accumulator D from TMEM -- 16 B per amplitude for the per-tile kernel (64 fp32
+    # columns per 16-amplitude row), 8 B for the persistent kernel (32 columns) -- against
+    # the measured tcgen05.ld throughput, 415 B/cycle/SM with 8 warps x 4 CTAs
+    # (profiles/r2_ubench_sm.txt; the B300 table's 64 B/cycle does not hold on B200)
     if args.tensor_cores_on:
         fused = sum(s["fused_gates"] for s in stats)
-        tmem_bytes = fused * (1 << N_QUBITS) * 16.0
-        tmem_peak = 64.0 * 148 * mhz * 1e6 / 1e9
+        bpa = 8 if pinfo["kernel"] == 13 else 16
+        tmem_bytes = fused * (1 << N_QUBITS) * float(bpa)
+        tmem_peak = 415.0 * 148 * mhz * 1e6 / 1e9
         tmem_gbs = tmem_bytes / (pass_ms / 1e3) / 1e9
         roof["tmem_read"] = {"achieved_gbs": tmem_gbs, "peak_gbs": tmem_peak, "frac": tmem_gbs / tmem_peak,
-                             "bytes_per_amplitude_gate": 16,
-                             "peak_source": f"derived: 64 B/cycle/SM (B300_MICROARCH LDTM) x 148 SM x {mhz:.0f} MHz",
-                             "note": "per-gate marginal cost of chained f16 gates = 2^(n+4) B / this peak"}
+                             "bytes_per_amplitude_gate": bpa,
+                             "peak_source": f"measured: 415 B/cycle/SM tcgen05.ld (profiles/r2_ubench_sm.txt) x 148 SM x {mhz:.0f} MHz"}
     # traffic: DRAM bytes per launch from the committed ncu --set full capture,
     # scaled to this run's average launch (ratio dram/algorithmic of that capture)
-    tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r2_traffic.json")
+    if not os.path.exists(tpath):
+        tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
     if os.path.exists(tpath):
         tr = json.load(open(tpath))
         roof["traffic"] = tr["ratio"] * alg_bytes / max(pass_launches, 1)
         roof["traffic_unit"] = "bytes/launch"
         roof["traffic_source"] = tr["source"]
     roof["alg_bytes_per_launch"] = alg_bytes / max(pass_launches, 1)
-    roof["kernel"] = ("tile_pass_kernel<12,%d,tensor-core,%d>" % ((5, 5) if args.fuse > 4 else (5, 4))
-                      if args.tensor_cores_on else "tile_pass_kernel<12,4> (CUDA cores)")
+    roof["kernel"] = ("tile_pass_v2_kernel (persistent TMEM kernel, 13-qubit tiles)" if pinfo["kernel"] == 13 else
+                      ("tile_pass_kernel<12,5,tensor-core,%d>" % pinfo["kernel"]) if pinfo["kernel"] else
+                      "tile_pass_kernel<12,4> (CUDA cores)")
     roof["launches_timed"] = int(pass_launches)
     roof["avg_launch_ms"] = pass_ms / max(pass_launches, 1)
     roof["share_of_step"] = pass_ms / tot_ms if tot_ms else None
@@ -337,10 +428,14 @@ def bench_gpu(args):
     # ---- gate-pass HBM GB/s vs peak (second half of the metric; SURVEY 8(d) C4 sweep
     # at n = sweep_n): one fused k-qubit Haar gate per HBM sweep, 2^(n+4) bytes per pass
     sweep = None
+    extra = {}
     if rank == 0 and args.sweep_n > 0:
         del state
         torch.cuda.empty_cache()
         sweep = gate_pass_sweep(ctx, args.sweep_n, dev, hbm_peak)
+        torch.cuda.empty_cache()
+    if rank == 0 and not args.no_configs:
+        extra = other_configs(ctx, dev, host_threads)
 
     # ---- CPU oracle baseline (rank 0, N = 1 only, bounded sample)
     cpu = None
@@ -354,11 +449,14 @@ def bench_gpu(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (complex64 state; fp64 reductions)",
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "complex64 state; gate products as f16 hi/lo splits (x_hi W_hi + x_lo W_hi + x_hi W_lo, "
+                     "~22-bit), fp32 accumulate; fp64 reductions",
             "data": "synthetic (seeded C2 generator; SURVEY 8(d))",
             "config": {"workload": "C2 20q sycamore-grid depth14 QCS-noise",
                        "trajectories_per_step": TOTAL_TRAJ * world, "trajectories_per_gpu": TOTAL_TRAJ,
-                       "n_qubits": N_QUBITS, "max_fused": args.fuse, "tile_bits": 12, "batch": batch,
+                       "n_qubits": N_QUBITS, "max_fused": args.fuse, "tile_bits": int(pinfo["tile_bits"]),
+                       "batch": batch,
                        "shots_per_traj": 1, "observables": len(obs), "parallelism": f"traj{world}",
                        "host_threads_per_rank": host_threads,
                        "l2": "flushed between timed steps (512 MB write)"},
@@ -367,6 +465,12 @@ def bench_gpu(args):
             "roofline": roof,
             "cpu_baseline": cpu,
             "gate_pass_sweep": sweep,
+            "strong": strong,
+            "plan": {"core_ms_per_traj": plan_core_ms, "wall_ms_per_step": st["plan_ms"],
+                     "host_threads": host_threads, "device_ms_per_step": st["device_ms"],
+                     "hidden": st["plan_ms"] < st["device_ms"],
+                     "note": "planning of batch i+1 overlaps batch i on the device; core_ms = one host core"},
+            "c1": extra.get("c1"), "c3": extra.get("c3"), "c4": extra.get("c4"),
             "clocks": clocks,
             "per_step_stats": {"passes_per_traj": st["passes"] / max(st["trajectories"], 1),
                                "fused_gates_per_traj": st["fused_gates"] / max(st["trajectories"], 1),
@@ -392,7 +496,8 @@ def main():
     ap.add_argument("--tensor-cores", type=int, default=0, help="0 auto, 1 on, -1 CUDA-core K1")
     ap.add_argument("--batch", type=int, default=384)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--sweep-n", type=int, default=30, help="qubits of the gate-pass bandwidth sweep (0 = skip)")
+    ap.add_argument("--sweep-n", type=int, default=32, help="qubits of the gate-pass bandwidth sweep (0 = skip)")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C1 / C3 / C4 extra keys")
     args = ap.parse_args()
     global TENSOR_CORES
     TENSOR_CORES = args.tensor_cores

@@ -251,6 +251,32 @@ qt_status qt_channel_choose(int nq, int n_kraus, const double* K, const int* qub
  *   bit.  p00_err / p11_err: n doubles or NULL.  In place; host only. */
 qt_status qt_readout_flips(int n, const double* p00_err, const double* p11_err, uint64_t seed, uint64_t traj,
                            int nshots, const int32_t* shot_ids, uint64_t* bits);
+/* Host-side arithmetic of the distributed-state mode (distributed.py orchestrates;
+ * these compute).  All host only; inputs are copied / read, outputs caller-owned.
+ * qt_rank_sample: the chain-rule levels n_total-1 .. n_local (reading R13) over the
+ *   rank bits: level l is held by rank bit level_rank_bit[l - n_local]; the masses
+ *   of the two children are sums of rank_mass[r] over the candidate ranks in
+ *   ascending r; the SAMPLE draw of (shot_ids[i], l) decides; out_prefix[i] = the
+ *   chosen high bits (bit l = logical level l), out_owner[i] = the rank that holds
+ *   the chosen slice (it samples the local levels with qt_sample_local).
+ *   world = 2^(n_total - n_local).
+ * qt_restrict_diagonal: a diagonal operator diag (2^nq complex, Kronecker order of
+ *   its listed qubits) on a rank where listed qubit m is global with value fixed[m]
+ *   (0 / 1) or local (fixed[m] = -1): out = the 2^k diagonal over the k local
+ *   qubits (listed order, Kronecker), *out_k = k (k = 0: a scalar on this rank).
+ * qt_embed_rho_diagonal: rho_Q (2^nq x 2^nq complex, internal order: bit m <->
+ *   m-th lowest position) of a channel whose K_i^dag K_i are all diagonal (P:204-212
+ *   then read only diag rho_Q), on one rank: position m is global with value
+ *   global_bit[m] or local (-1); diag_local = the 2^n_loc diagonal of the rank's
+ *   reduced rho over its local positions (ascending), or its norm when n_loc = 0.
+ * qt_channel_operator: the operator a pick applies, out = K_pick * scale (Alg. 2
+ *   line 7 deferred pick / line 16 conventional pick, P:197 / P:207). */
+qt_status qt_rank_sample(int world, const double* rank_mass, int n_total, int n_local, const int* level_rank_bit,
+                         uint64_t seed, uint64_t traj, int nshots, const int32_t* shot_ids, uint64_t* out_prefix,
+                         int32_t* out_owner);
+qt_status qt_restrict_diagonal(int nq, const double* diag, const int* fixed, double* out, int* out_k);
+qt_status qt_embed_rho_diagonal(int nq, const int* global_bit, int n_loc, const double* diag_local, double* out);
+qt_status qt_channel_operator(int nq, int n_kraus, const double* K, int pick, double scale, double* out);
 qt_status qt_apply_plan(qt_ctx ctx, qt_plan plan, void* state_dev, size_t state_bytes);
 qt_status qt_reduce_rho(qt_ctx ctx, const void* state_dev, int n, int nq, const int* qubits, double* out);
 qt_status qt_sample_local(qt_ctx ctx, const void* state_dev, int n, int n_total, uint64_t seed, uint64_t traj,
@@ -262,7 +288,10 @@ qt_status qt_expectation_partials(qt_ctx ctx, const void* state_dev, int n, int 
  * `traj` exactly as qt_run_trajectories would and reports
  * out[0] tile passes, [1] fused gates, [2] conventional channels (rho_Q
  * reductions), [3] deferred picks, [4] conventional picks, [5] matrix-pool
- * entries, [6] algorithmic bytes, [7] fused-gate constituents. */
+ * entries, [6] algorithmic bytes, [7] fused-gate constituents, [8] tile bits T,
+ * [9] K1 kernel: 0 CUDA cores, 4 / 5 / 6 per-tile tensor-core kernel for gates
+ * padded to that many qubits, 13 persistent TMEM kernel (13-qubit tiles).
+ * out holds 10 int64. */
 qt_status qt_plan_info(qt_plan plan, uint64_t seed, uint64_t traj, int64_t* out);
 
 /* Lower bound used by the sampler, exposed for tests: sigma_min(K)^2 of a

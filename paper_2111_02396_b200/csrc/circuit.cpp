@@ -453,9 +453,9 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
     // default for n >= 13 (tile_bits 0 or 13); tile_bits = 12 selects the per-tile kernel
     const bool v2_ok = C.n >= 13 && o.tensor_cores >= 0 && f <= 4 && max_arity <= f &&
                        (o.tile_bits == 0 || o.tile_bits == 13) && o.low_bits == 0;
-    // (default while the persistent kernel is being tuned: opt in with QT_TILE13=1 or tile_bits = 13)
+    // (QT_TILE13=0 selects the per-tile kernel instead, for A/B measurements)
     const char* env13 = std::getenv("QT_TILE13");
-    const bool auto13 = env13 && env13[0] == '1';
+    const bool auto13 = !(env13 && env13[0] == '0');
     P.T = o.tile_bits ? o.tile_bits : std::min(C.n, (v2_ok && auto13) ? 13 : 12);
     if (P.T == 13 && !v2_ok) {
         delete hp;

@@ -44,15 +44,9 @@ std::vector<std::vector<int>> fuse_items(const std::vector<FuseItem>& items, int
             on_q[q].push_back(i);
         }
     }
-    auto qubit_at = [&](int i, int m) {
-        uint64_t mk = items[i].mask;
-        for (int k = 0; k < m; ++k) mk &= mk - 1;
-        return __builtin_ctzll(mk);
-    };
     // ---- phase 1: absorb small items into time-adjacent larger ones on the same qubits
     std::vector<int> group(N);
     for (int i = 0; i < N; ++i) group[i] = i;
-    std::vector<int> big(N, 0);  // group anchor flags
     auto k_of = [&](int g) { return popc(items[g].mask); };
     std::vector<char> absorbed(N, 0);
     // forward absorption (an item joins the next larger item on all of its qubits); reverse order
@@ -97,8 +91,6 @@ std::vector<std::vector<int>> fuse_items(const std::vector<FuseItem>& items, int
         absorbed[i] = 1;
         has_members[G] = 1;
     }
-    (void)big;
-    (void)qubit_at;
     // groups: anchor id -> members (time order)
     std::vector<int> gid(N, -1);
     std::vector<std::vector<int>> members;

@@ -835,6 +835,9 @@ qt_status qt_apply_gate_ex(qt_ctx ctx, void* state_dev, int n, int nq, const int
     }
     qt_fuse_opts o{};
     o.max_fused = std::max(nq, 2);
+    // one fused gate per HBM pass: the per-tile kernel (12-qubit tiles) streams these faster
+    // than the persistent kernel, whose strength is long in-TMEM gate chains
+    if (n >= 12) o.tile_bits = 12;
     qt_plan p = nullptr;
     e = qt_fuse_ex(c, &o, &p);
     qt_circuit_destroy(c);
@@ -868,6 +871,8 @@ qt_status qt_plan_info(qt_plan plan, uint64_t seed, uint64_t traj, int64_t* out)
     out[5] = (int64_t)pg.pool_size;
     out[6] = (int64_t)pg.alg_bytes;
     out[7] = (int64_t)pg.cons.size();
+    out[8] = P.T;
+    out[9] = P.v2 ? 13 : (P.tc ? P.tc_k : 0);
     return QT_OK;
 }
 

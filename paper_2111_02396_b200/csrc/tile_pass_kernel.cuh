@@ -887,6 +887,7 @@ tile_pass_kernel(const TileArgs A, const int step) {
         // flushed with one barrier pair per 64 / warps observables
         constexpr int NW = (NT + 31) / 32;
         constexpr int kFlush = 64 / NW;
+        __syncthreads();  // red[] may still be read by a preceding block sum (racecheck)
         for (int o = 0; o < P.obs_count; ++o) {
             const ObsDesc O = A.obs[P.obs_begin + o];
             const uint32_t zl = to_local<T>(O.zmask, P);

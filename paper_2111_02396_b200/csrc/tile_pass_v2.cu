@@ -473,9 +473,10 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
             issue_w();
             issue_w();
             const uint64_t base = cx->base, base3 = cx->base3;
-            // one thread polls the tile's mbarrier; the others sleep in the barrier
-            if (elect) mbar_wait_s(full_bar(b), (uint32_t)((jj / NBUF) & 1));
-            bar_wg(wg);
+            // every thread acquires the tile's "full" phase (the cp.async writes of the
+            // loading warpgroup; a single poller + bar.sync would order them too, but
+            // compute-sanitizer racecheck only tracks the direct acquire)
+            mbar_wait_s(full_bar(b), (uint32_t)((jj / NBUF) & 1));
             QT_T(0);
             float run_inv = 1.f;
             for (int g = 0; g < ng;) {

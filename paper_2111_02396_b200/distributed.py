@@ -160,6 +160,9 @@ class TorchFabric:
         self.rank = dist.get_rank(group)
         self.local_ranks = [self.rank]
         self.device = device
+        # gloo moves CPU tensors only: CUDA states are staged through the host (the
+        # 2-process single-GPU test; NCCL moves device memory directly over NVLink)
+        self.stage_host = dist.get_backend(group) == "gloo"
 
     def exchange_top(self, states, gbits, s, pool=None):
         # chunk c goes to rank _dest(c) and arrives at chunk _src_chunk(source):
@@ -176,7 +179,13 @@ class TorchFabric:
             out_split[_dest(self.rank, gbits, c)] = chunk
         # receive into the backend's spare buffer; the sent buffer becomes the spare
         y = pool.take_spare(x) if hasattr(pool, "take_spare") else self.torch.empty_like(x)
-        self.dist.all_to_all_single(y, x.contiguous(), out_split, in_split, group=self.group)
+        if self.stage_host and x.is_cuda:
+            xc = x.contiguous().cpu()
+            yc = self.torch.empty_like(xc)
+            self.dist.all_to_all_single(yc, xc, out_split, in_split, group=self.group)
+            y.copy_(yc)
+        else:
+            self.dist.all_to_all_single(y, x.contiguous(), out_split, in_split, group=self.group)
         if hasattr(pool, "give_spare"):
             pool.give_spare(x)
         return {self.rank: y}
@@ -259,24 +268,13 @@ class DistributedTrajectory:
     def _push_diag_global(self, qubits, M):
         """A diagonal operator touching global qubits, applied without a swap:
         on rank r it is the diagonal restricted to r's values of the global
-        qubits, i.e. an operator on the local qubits only (or a scalar)."""
-        M = np.asarray(M, np.complex128)
-        nq = len(qubits)
-        d = np.diag(M)
+        qubits, i.e. an operator on the local qubits only (or a scalar)
+        (qt_restrict_diagonal)."""
+        d = np.diag(np.asarray(M, np.complex128))
         loc = [m for m, q in enumerate(qubits) if self.slot[q] < self.nl]
         for r in self.f.local_ranks:
-            gval = {m: (r >> (self.slot[q] - self.nl)) & 1 for m, q in enumerate(qubits) if self.slot[q] >= self.nl}
-            k = len(loc)
-            dd = np.zeros(1 << k, np.complex128)
-            for a in range(1 << k):
-                idx = 0
-                for m in range(nq):
-                    if m in gval:
-                        bit = gval[m]
-                    else:
-                        bit = (a >> (k - 1 - loc.index(m))) & 1
-                    idx |= bit << (nq - 1 - m)
-                dd[a] = d[idx]
+            fixed = [(r >> (self.slot[q] - self.nl)) & 1 if self.slot[q] >= self.nl else -1 for q in qubits]
+            dd, k = qtraj.restrict_diagonal(d, fixed)
             if k == 0:  # a scalar on this rank
                 if dd[0] != 1.0:
                     self.pending_all.append((r, [0], np.diag([dd[0], dd[0]])))
@@ -345,31 +343,21 @@ class DistributedTrajectory:
 
     def _rho_diag_global(self, qubits: Sequence[int]):
         """Diagonal of rho_Q over qubits some of which are global: rank r holds
-        the entries whose global bits equal r's.  Returns per-rank matrices in
-        the internal order of the sorted slot positions, and those positions."""
+        the entries whose global bits equal r's (qt_embed_rho_diagonal).  Returns
+        per-rank matrices in the internal order of the sorted slot positions, and
+        those positions."""
         pos = [self.slot[q] for q in qubits]
         order = sorted(pos)
-        d = 1 << len(pos)
         loc = [p for p in order if p < self.nl]
         out = {}
         for rk in self.f.local_ranks:
-            rho = np.zeros((d, d), np.complex128)
             if loc:
-                rl = self.b.reduce_rho(self.states[rk], loc)
-                diag_l = np.real(np.diag(rl))
+                diag_l = np.real(np.diag(self.b.reduce_rho(self.states[rk], loc)))
             else:
                 _, norm = self.b.expect(self.states[rk], [])
                 diag_l = np.array([norm])
-            for a_l in range(1 << len(loc)):
-                a = 0
-                for m, p in enumerate(order):
-                    if p < self.nl:
-                        bit = (a_l >> loc.index(p)) & 1
-                    else:
-                        bit = (rk >> (p - self.nl)) & 1
-                    a |= bit << m
-                rho[a, a] = diag_l[a_l]
-            out[rk] = rho
+            gbits = [(rk >> (p - self.nl)) & 1 if p >= self.nl else -1 for p in order]
+            out[rk] = qtraj.embed_rho_diagonal(gbits, diag_l)
         return out, pos
 
     def _pauli_values(self, strings: Sequence[str]) -> np.ndarray:
@@ -437,7 +425,9 @@ class DistributedTrajectory:
             upcoming = uses[i + 1:i + 1 + lookahead]
             touches_global = any(self.slot[q] >= self.nl for q in op.qubits)
             if not hasattr(op, "kraus"):
-                M = np.asarray(op.matrix, np.complex128)
+                # sweep gates: parameter set traj mod n_sets, as in qt_run_trajectories
+                mats = getattr(op, "matrices", None)
+                M = np.asarray(mats[traj % len(mats)] if mats is not None else op.matrix, np.complex128)
                 if touches_global and _is_diag(M):
                     self._push_diag_global(op.qubits, M)
                 else:
@@ -459,14 +449,15 @@ class DistributedTrajectory:
                     rho = {rk: self.b.reduce_rho(self.states[rk], pos) for rk in self.f.local_ranks}
                 tot = self.f.allreduce(rho)
                 pick, sc = qtraj.channel_choose(op.kraus, pos, tot, r, self.mode)
-            M = np.asarray(op.kraus[pick], np.complex128) * sc
+            M = qtraj.channel_operator(op.kraus, pick, sc)
             if not _is_identity(M):
                 if any(self.slot[q] >= self.nl for q in op.qubits) and _is_diag(M):
                     self._push_diag_global(op.qubits, M)
                 else:
                     self._ensure_local(op.qubits, upcoming)
                     self._push([self.slot[q] for q in op.qubits], M)
-            kraus_rec.append(pick)
+            if getattr(op, "record", True):  # keyed channels only, as qt_run_trajectories records them
+                kraus_rec.append(pick)
             ch += 1
         self._flush()
         out = {"kraus": np.array(kraus_rec, np.int32)}
@@ -502,28 +493,12 @@ class DistributedTrajectory:
             _, norm = self.b.expect(self.states[rk], [])
             masses[rk] = norm if norm > 0.0 else 0.0
         M = self.f.allgather(masses)
-        # chain rule over the rank bits (levels n-1 .. nl), then local levels on the owner
-        half_n = (self.n + 1) // 2
-        bits = np.zeros(shots, np.uint64)
-        owners = np.zeros(shots, np.int64)
-        for sh in range(shots):
-            prefix = 0          # logical high bits chosen so far
-            cand = list(range(self.f.world))
-            for lvl in range(self.n - 1, self.nl - 1, -1):
-                gb = self.slot[lvl] - self.nl
-                m0 = sum(M[r] for r in cand if not (r >> gb) & 1)
-                m1 = sum(M[r] for r in cand if (r >> gb) & 1)
-                u = qtraj.draw(seed, sh * half_n + lvl // 2, PURPOSE_SAMPLE, traj, lvl & 1)
-                if m0 == 0.0:
-                    bit = 1
-                elif m1 == 0.0:
-                    bit = 0
-                else:
-                    bit = 0 if u * (m0 + m1) < m0 else 1
-                cand = [r for r in cand if ((r >> gb) & 1) == bit]
-                prefix |= bit << lvl
-            owners[sh] = cand[0]
-            bits[sh] = prefix
+        # chain rule over the rank bits (levels n-1 .. nl; qt_rank_sample), then the
+        # local levels on the owner
+        level_bit = [self.slot[lvl] - self.nl for lvl in range(self.nl, self.n)]
+        bits, owners = qtraj.rank_sample([M[r] for r in range(self.f.world)], self.n, self.nl, level_bit, seed, traj,
+                                         np.arange(shots, dtype=np.int32))
+        bits = bits.astype(np.uint64)
         for rk in self.f.local_ranks:
             ids = [sh for sh in range(shots) if owners[sh] == rk]
             if ids:

@@ -85,6 +85,11 @@ def lib() -> ctypes.CDLL:
         "qt_readout_flips": ([ctypes.c_int, dp, dp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ip,
                               ctypes.POINTER(ctypes.c_uint64)], ctypes.c_int),
         "qt_circuit_num_sets": ([vp], ctypes.c_int),
+        "qt_rank_sample": ([ctypes.c_int, dp, ctypes.c_int, ctypes.c_int, ip, ctypes.c_uint64, ctypes.c_uint64,
+                            ctypes.c_int, ip, ctypes.POINTER(ctypes.c_uint64), ip], ctypes.c_int),
+        "qt_restrict_diagonal": ([ctypes.c_int, dp, ip, dp, ip], ctypes.c_int),
+        "qt_embed_rho_diagonal": ([ctypes.c_int, ip, ctypes.c_int, dp, dp], ctypes.c_int),
+        "qt_channel_operator": ([ctypes.c_int, ctypes.c_int, dp, ctypes.c_int, ctypes.c_double, dp], ctypes.c_int),
         "qt_circuit_num_channels": ([vp], ctypes.c_int),
         "qt_fuse": ([vp, ctypes.c_int, ctypes.POINTER(vp)], ctypes.c_int),
         "qt_fuse_ex": ([vp, ctypes.POINTER(FuseOpts), ctypes.POINTER(vp)], ctypes.c_int),
@@ -238,9 +243,10 @@ class Plan:
 
     def info(self, seed: int, traj: int) -> dict:
         """Host-only planning of one trajectory: pass / gate / event counts."""
-        out = (ctypes.c_int64 * 8)()
+        out = (ctypes.c_int64 * 10)()
         _check(lib().qt_plan_info(self.h, seed, traj, out))
-        keys = ["passes", "fused_gates", "events", "deferred", "conventional", "pool", "alg_bytes", "constituents"]
+        keys = ["passes", "fused_gates", "events", "deferred", "conventional", "pool", "alg_bytes", "constituents",
+                "tile_bits", "kernel"]
         return dict(zip(keys, list(out)))
 
     def __del__(self):
@@ -387,6 +393,51 @@ def readout_flips(bits: np.ndarray, n: int, p00, p11, seed: int, traj: int, shot
     _check(lib().qt_readout_flips(n, None if a is None else _dptr(a), None if b is None else _dptr(b), seed, traj,
                                   len(out), _iptr(ids), out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
     return out
+
+
+def rank_sample(rank_mass, n_total: int, n_local: int, level_rank_bit, seed: int, traj: int, shot_ids):
+    """Chain rule over the rank bits (qt_rank_sample): (prefix bits, owner rank) per shot."""
+    m = np.ascontiguousarray(rank_mass, np.float64)
+    lv = np.ascontiguousarray(level_rank_bit, np.int32)
+    ids = np.ascontiguousarray(shot_ids, np.int32)
+    pre = np.zeros(len(ids), np.uint64)
+    own = np.zeros(len(ids), np.int32)
+    _check(lib().qt_rank_sample(len(m), _dptr(m), n_total, n_local, _iptr(lv), seed, traj, len(ids), _iptr(ids),
+                                pre.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), _iptr(own)))
+    return pre, own
+
+
+def restrict_diagonal(diag, fixed):
+    """Diagonal operator restricted to one rank's global-qubit values (qt_restrict_diagonal):
+    the diagonal over the local listed qubits (empty shape () -> a scalar)."""
+    d = np.ascontiguousarray(np.asarray(diag, np.complex128)).view(np.float64)
+    fx = np.ascontiguousarray(fixed, np.int32)
+    out = np.zeros(2 * len(d) // 2, np.float64)
+    k = ctypes.c_int(0)
+    _check(lib().qt_restrict_diagonal(len(fx), _dptr(d), _iptr(fx), _dptr(out), ctypes.byref(k)))
+    return out.view(np.complex128)[: 1 << k.value], k.value
+
+
+def embed_rho_diagonal(global_bit, diag_local):
+    """rho_Q of a diagonal-K^dag K channel from a rank's local diagonal (qt_embed_rho_diagonal)."""
+    gb = np.ascontiguousarray(global_bit, np.int32)
+    dl = np.ascontiguousarray(np.real(np.asarray(diag_local)), np.float64).reshape(-1)
+    nq = len(gb)
+    out = np.zeros(2 << (2 * nq), np.float64)
+    _check(lib().qt_embed_rho_diagonal(nq, _iptr(gb), int((gb < 0).sum()), _dptr(dl), _dptr(out)))
+    d = 1 << nq
+    return out.view(np.complex128).reshape(d, d)
+
+
+def channel_operator(kraus, pick: int, scale: float) -> np.ndarray:
+    """K_pick * scale (qt_channel_operator)."""
+    ks = list(kraus)
+    nq = int(np.log2(np.asarray(ks[0]).shape[0]))
+    m = np.concatenate([_cplx(k) for k in ks])
+    out = np.zeros(2 << (2 * nq), np.float64)
+    _check(lib().qt_channel_operator(nq, len(ks), _dptr(m), pick, scale, _dptr(out)))
+    d = 1 << nq
+    return out.view(np.complex128).reshape(d, d)
 
 
 def channel_first_loop(kraus, u: float, mode: int = 0):

@@ -213,3 +213,55 @@ def test_gpu_backend_emulated_fabric_matches_oracle(world):
         bad = [s for s in range(3) if out["bits"][s] != ref["bits"][t][s] and ref["sample_margin"][t][s] >= 1e-4]
         assert not bad
         assert np.max(np.abs(out["obs"] - ref["obs"][t])) < 1e-4
+
+
+def _gpu_gloo_worker(rank, port, q, world, n):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ctx = qtraj.Context(0)
+    c = circuit(n, seed=41, noise="ad")
+    c.observables += ["I" * (n - 1) + "X", "Y" + "I" * (n - 3) + "ZX"]
+    res = []
+    for t in range(2):
+        tr = D.DistributedTrajectory(D.GpuBackend(ctx, "cuda:0"), D.TorchFabric(), n)
+        out = tr.run(c, seed=91, traj=t, shots=3, observables=c.observables)
+        res.append({k: np.asarray(v) for k, v in out.items() if k in ("kraus", "bits", "obs", "sample_margin")})
+    q.put((rank, res))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gpu_backend_torch_fabric_two_processes():
+    """The production pairing GpuBackend + TorchFabric: two processes (ranks) on one GPU,
+    gloo all-to-all with the CUDA states staged through the host (NCCL on multi-GPU
+    nodes); both ranks reproduce the oracle's trajectories."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import multiprocessing as mp
+    n, world = 14, 2
+    mctx = mp.get_context("spawn")
+    q = mctx.Queue()
+    port = _free_port()
+    ps = [mctx.Process(target=_gpu_gloo_worker, args=(r, port, q, world, n)) for r in range(world)]
+    for p in ps:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(world))
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    c = circuit(n, seed=41, noise="ad")
+    c.observables += ["I" * (n - 1) + "X", "Y" + "I" * (n - 3) + "ZX"]
+    ref = oracle.run_trajectories(c, seed=91, traj_count=2, shots=3)
+    for rank in range(world):
+        for t in range(2):
+            out = got[rank][t]
+            assert (out["kraus"] == ref["kraus"][t]).all()
+            bad = [s for s in range(3) if out["bits"][s] != ref["bits"][t][s] and ref["sample_margin"][t][s] >= 1e-4]
+            assert not bad
+            assert np.max(np.abs(out["obs"] - ref["obs"][t])) < 1e-4
