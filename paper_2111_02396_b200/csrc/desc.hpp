@@ -27,7 +27,9 @@ struct PassDesc {
     int32_t obs_count;
     uint8_t tq[16];       // global qubit of tile bit i (ascending), i < T
     int32_t slot;         // batch slot (set by the executor in the per-step launch arrays)
-    int32_t pad[3];
+    uint32_t rho_local = 0;  // kPassRho: the channel's qubits as tile-local bits
+    int32_t rho_nq = 0;      // kPassRho: channel arity
+    int32_t pad = 0;
 };
 static_assert(sizeof(PassDesc) == 64, "PassDesc layout");
 

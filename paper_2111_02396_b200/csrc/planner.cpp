@@ -938,6 +938,16 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
         for (size_t pi : seg_pass_idx) {
             PassDesc& pd = out.passes[pi];
             pd.tile_mask = fill_tile(pd.tile_mask, T, n);
+            pd.rho_local = 0;
+            pd.rho_nq = 0;
+            pd.pad = 0;
+            if (pd.flags & kPassRho) {
+                const uint64_t qm = barriers[si].qmask;
+                int i = 0;
+                for (uint64_t mk = pd.tile_mask; mk; mk &= mk - 1, ++i)
+                    if ((qm >> __builtin_ctzll(mk)) & 1u) pd.rho_local |= 1u << i;
+                pd.rho_nq = popc(qm);
+            }
             for (int g = 0; g < pd.gate_count; ++g) {
                 GateDesc& gd = out.gates[pd.gate_begin + g];
                 // 6-qubit tensor-core gates: every gate bit in registers (R = 6)

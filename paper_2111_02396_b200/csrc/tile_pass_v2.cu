@@ -177,19 +177,60 @@ __device__ __forceinline__ void wg_sum_n(double (&v)[N], double* red, int wg) {
     }
 }
 
-// rho_Q partial (2^Q x 2^Q, fp64) of the tile for a channel at tile-local bits qlocal.
+// Warp reduce-scatter of NE values (NE a power of two <= 32), fixed order: after
+// log2(NE) halving exchanges lane l holds the warp sum of value l >> (5 - log2 NE)
+// (the remaining lane bits then reduce by xor pairs, a + b == b + a bit for bit).
+template <int NE>
+__device__ __forceinline__ double warp_reduce_scatter(double (&v)[NE], int lane) {
+    int o = 16;
+#pragma unroll
+    for (int h = NE / 2; h >= 1; h >>= 1, o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+            const double send = up ? v[i] : v[i + h];
+            const double keep = up ? v[i + h] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    double r = v[0];
+#pragma unroll
+    for (; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    return r;
+}
+
+// rho_Q partial (2^Q x 2^Q, fp64) of the tile for a channel at tile-local bits qlocal
+// (rho_Q = sum over the other qubits of psi psi^dag).  Only the upper
+// triangle is accumulated -- D real diagonal entries, then (re, im) of (a, b), a < b --
+// and the lower one written as its conjugate.  Every thread takes TILE / D / NT
+// complementary indices (the tile index with zeros inserted at the channel bits), so
+// no thread idles; the warpgroup sum is a reduce-scatter per warp, then a fixed-order
+// sum over the 8 warps.
 template <int Q>
 __device__ __forceinline__ void rho_partial(const float2* tile, uint32_t qlocal, double* out, double* red, int wg) {
     constexpr int D = 1 << Q;
-    const int wtid = threadIdx.x & (NT - 1);
+    constexpr int NE = D * D;
+    const int wtid = threadIdx.x & (NT - 1), lane = wtid & 31;
     uint32_t qoff[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) qoff[a] = pdep32((uint32_t)a, qlocal);
-    double acc[2 * D * D];
+    uint32_t qp[Q];
+    {
+        uint32_t m = qlocal;
 #pragma unroll
-    for (int e = 0; e < 2 * D * D; ++e) acc[e] = 0.0;
-    for (uint32_t bL = wtid; bL < (uint32_t)TILE; bL += NT) {
-        if (bL & qlocal) continue;
+        for (int q = 0; q < Q; ++q) {
+            qp[q] = (uint32_t)__ffs(m) - 1u;
+            m &= m - 1u;
+        }
+    }
+    double acc[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) acc[e] = 0.0;
+#pragma unroll 2
+    for (uint32_t k = wtid; k < (uint32_t)(TILE >> Q); k += NT) {
+        uint32_t bL = k;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) bL = (bL & ((1u << qp[q]) - 1u)) | ((bL >> qp[q]) << (qp[q] + 1u));
         double vr[D], vi[D];
 #pragma unroll
         for (int a = 0; a < D; ++a) {
@@ -197,18 +238,46 @@ __device__ __forceinline__ void rho_partial(const float2* tile, uint32_t qlocal,
             vr[a] = v.x;
             vi[a] = v.y;
         }
+        int e = 0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) acc[e++] += vr[a] * vr[a] + vi[a] * vi[a];
 #pragma unroll
         for (int a = 0; a < D; ++a)
 #pragma unroll
-            for (int b = 0; b < D; ++b) {
-                acc[2 * (a * D + b)] += vr[a] * vr[b] + vi[a] * vi[b];
-                acc[2 * (a * D + b) + 1] += vi[a] * vr[b] - vr[a] * vi[b];
+            for (int b = a + 1; b < D; ++b) {
+                acc[e++] += vr[a] * vr[b] + vi[a] * vi[b];
+                acc[e++] += vi[a] * vr[b] - vr[a] * vi[b];
             }
     }
-    wg_sum_n<2 * D * D>(acc, red, wg);
-    if (wtid == 0)
+    const double r = warp_reduce_scatter<NE>(acc, lane);
+    bar_wg(wg);  // previous readers of red are done
+    if ((lane & (32 / NE - 1)) == 0) red[(wtid >> 5) * NE + (lane / (32 / NE))] = r;
+    bar_wg(wg);
+    if (wtid < NE) {
+        double v = 0.0;
 #pragma unroll
-        for (int e = 0; e < 2 * D * D; ++e) out[e] = acc[e];
+        for (int w = 0; w < NWW; ++w) v += red[w * NE + wtid];
+        // entry wtid of the compact order -> (a, b) and its mirror
+        if (wtid < D) {
+            out[2 * (wtid * D + wtid)] = v;
+            out[2 * (wtid * D + wtid) + 1] = 0.0;
+        } else {
+            int e = D, a = 0, b = 1;
+            for (; e + 2 <= wtid; e += 2) {
+                if (++b == D) {
+                    ++a;
+                    b = a + 1;
+                }
+            }
+            if (wtid == e) {
+                out[2 * (a * D + b)] = v;
+                out[2 * (b * D + a)] = v;
+            } else {
+                out[2 * (a * D + b) + 1] = v;
+                out[2 * (b * D + a) + 1] = -v;
+            }
+        }
+    }
 }
 
 // 3-qubit channels: one row of rho_Q at a time.
@@ -433,8 +502,11 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
         atomicAdd(A.timing + (k), (unsigned long long)(t_now - t_prev));                     \
         t_prev = t_now;                                                                      \
     }
+#define QT_C(k, v)                                                                           \
+    if (wtid == 0 && blockIdx.x == 7) atomicAdd(A.timing + (k), (unsigned long long)(v));
 #else
 #define QT_T(k)
+#define QT_C(k, v)
 #endif
         int kk = 0;  // this warpgroup's item count
         for (int jj = wg; raw(jj) < nitems; jj += 2, ++kk) {
@@ -478,6 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
             // compute-sanitizer racecheck only tracks the direct acquire)
             mbar_wait_s(full_bar(b), (uint32_t)((jj / NBUF) & 1));
             QT_T(0);
+            QT_C(11, 1);
             float run_inv = 1.f;
             for (int g = 0; g < ng;) {
                 if (!(gds[g].k & kGateTC)) {
@@ -537,6 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                     tc::fence_before();
                     bar_wg(wg);  // A complete; every fp32 read of this buffer done
                     QT_T(1);
+                    QT_C(13, 1);
                 }
                 // ---- the segment's gates ----
                 for (;;) {
@@ -561,6 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                         QT_T(7);
                     }
                     ++w_used;
+                    QT_C(12, 1);
                     const int32_t gk = gds[g].k;
                     __syncwarp();
                     if (prep_pending) {  // in the shadow of the MMAs
@@ -668,12 +743,10 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
             // ---------------- epilogues (read-only on the fp32 tile) ----------------
             const uint64_t tile_row = (uint64_t)slot * ntiles + tile_idx;
             if (P.flags & kPassRho) {
-                const EventDesc E = A.events[P.event];
-                const ChanDesc C = A.chans[E.chan];
-                const uint32_t ql = to_local<T>(C.qmask, P);
+                const uint32_t ql = P.rho_local;  // channel qubits as tile-local bits (planner)
                 double* out = A.rho_part + tile_row * A.rho_stride;
-                if (C.nq == 1) rho_partial<1>(tile, ql, out, red, wg);
-                else if (C.nq == 2) rho_partial<2>(tile, ql, out, red, wg);
+                if (P.rho_nq == 1) rho_partial<1>(tile, ql, out, red, wg);
+                else if (P.rho_nq == 2) rho_partial<2>(tile, ql, out, red, wg);
                 else rho_partial_rows3(tile, ql, out, red, wg);
                 __threadfence();
                 bar_wg(wg);
@@ -682,6 +755,8 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                 if (misc[1 + wg]) {
                     // last tile of the slot: sum the tile partials in a fixed order, then choose
                     __threadfence();
+                    const EventDesc E = A.events[P.event];
+                    const ChanDesc C = A.chans[E.chan];
                     const int ne = 2 * C.d * C.d;
                     double* fin = red + 128;  // ne <= 128 doubles: red[128..255] of this warpgroup
                     const double* part = A.rho_part + (uint64_t)slot * ntiles * A.rho_stride;
@@ -704,6 +779,8 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                         A.counters[slot] = 0;
                     }
                 }
+                QT_T(9);
+                QT_C(14, 1);
             }
             if (P.flags & kPassFinal) {
                 double s[1] = {0.0};
@@ -714,6 +791,8 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                 }
                 wg_sum_n<1>(s, red, wg);
                 if (wtid == 0) A.blocksum[tile_row] = s[0];
+                QT_T(10);
+                QT_C(15, 1);
             }
             if (P.flags & kPassObs) {
                 // Z strings: Walsh-Hadamard transform of |psi(wtid + m NT)|^2 over m
@@ -732,60 +811,79 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                             w[m] = a + c;
                             w[m | h] = a - c;
                         }
-                for (int o = 0; o < P.obs_count; ++o) {
-                    const ObsDesc O = A.obs[P.obs_begin + o];
-                    // tile-local Z bits (the final pass's tile is the low 13 qubits: a mask)
-                    const uint32_t zl = P.tile_mask == (uint64_t)(TILE - 1) ? (uint32_t)(O.zmask & (TILE - 1))
-                                                                             : to_local<T>(O.zmask, P);
-                    const int zs = __popcll(base & O.zmask) & 1;
-                    double part[1];
-                    if (O.xmask == 0) {
-                        const float vv = pick_uniform<NA>(w, (int)(zl >> 8));
-                        const int par = (__popc((uint32_t)wtid & zl & (uint32_t)(NT - 1)) + zs) & 1;
-                        part[0] = par ? -(double)vv : (double)vv;
-                    } else {
-                        const uint64_t xo = O.xmask & ~P.tile_mask;
-                        const uint32_t xl = to_local<T>(O.xmask, P);
-                        part[0] = 0.0;
-#pragma unroll 1
-                        for (int m = 0; m < NA; ++m) {
-                            const uint32_t L = (uint32_t)(wtid + m * NT);
-                            const float2 v = tile[swz(L)];
-                            float2 wv;
-                            if (xo == 0) {
-                                wv = tile[swz(L ^ xl)];
-                            } else {  // partner amplitude in another tile (read-only pass only)
-                                wv = st[(base + pdep64(L, P.tile_mask)) ^ O.xmask];
-                            }
-                            const double cr = (double)wv.x * v.x + (double)wv.y * v.y;
-                            const double ci = (double)wv.x * v.y - (double)wv.y * v.x;
-                            double t;
-                            switch (O.ny & 3) {
-                                case 0: t = cr; break;
-                                case 1: t = -ci; break;
-                                case 2: t = -cr; break;
-                                default: t = ci; break;
-                            }
-                            const int par = (__popc(L & zl) + zs) & 1;
-                            part[0] += par ? -t : t;
-                        }
+                // observable descriptors: lane l of every warp holds string o0 + l of the
+                // chunk, broadcast by shuffles (no dependent global load per string)
+                for (int o0 = 0; o0 < P.obs_count; o0 += 32) {
+                    uint64_t cx = 0, cz = 0;
+                    int cny = 0, cslot = 0;
+                    if (o0 + lane < P.obs_count) {
+                        const ObsDesc& Ol = A.obs[P.obs_begin + o0 + lane];
+                        cx = Ol.xmask;
+                        cz = Ol.zmask;
+                        cny = Ol.ny;
+                        cslot = Ol.slot;
                     }
-                    // warp sums parked per (observable, warp); one barrier pair per 16 strings,
-                    // then a fixed-order sum over the 8 warps
-#pragma unroll
-                    for (int sh = 16; sh > 0; sh >>= 1) part[0] += __shfl_xor_sync(0xffffffffu, part[0], sh);
-                    double* park = red + 128;  // 16 strings x 8 warps
-                    const int jo = o & 15;
-                    if (lane == 0) park[jo * NWW + (wtid >> 5)] = part[0];
-                    if (jo == 15 || o + 1 == P.obs_count) {
-                        bar_wg(wg);
-                        if (wtid <= jo) {
-                            double v = 0.0;
-#pragma unroll
-                            for (int w = 0; w < NWW; ++w) v += park[wtid * NWW + w];
-                            A.obs_part[tile_row * A.n_obs + A.obs[P.obs_begin + o - jo + wtid].slot] = v;
+                    const int oc = min(32, P.obs_count - o0);
+                    for (int j = 0; j < oc; ++j) {
+                        const int o = o0 + j;
+                        const uint64_t oxm = __shfl_sync(0xffffffffu, cx, j);
+                        const uint64_t ozm = __shfl_sync(0xffffffffu, cz, j);
+                        const int ony = __shfl_sync(0xffffffffu, cny, j);
+                        // tile-local Z bits (the final pass's tile is the low 13 qubits: a mask)
+                        const uint32_t zl = P.tile_mask == (uint64_t)(TILE - 1) ? (uint32_t)(ozm & (TILE - 1))
+                                                                                 : to_local<T>(ozm, P);
+                        const int zs = __popcll(base & ozm) & 1;
+                        double part[1];
+                        if (oxm == 0) {
+                            const float vv = pick_uniform<NA>(w, (int)(zl >> 8));
+                            const int par = (__popc((uint32_t)wtid & zl & (uint32_t)(NT - 1)) + zs) & 1;
+                            part[0] = par ? -(double)vv : (double)vv;
+                        } else {
+                            const uint64_t xo = oxm & ~P.tile_mask;
+                            const uint32_t xl = to_local<T>(oxm, P);
+                            part[0] = 0.0;
+#pragma unroll 1
+                            for (int m = 0; m < NA; ++m) {
+                                const uint32_t L = (uint32_t)(wtid + m * NT);
+                                const float2 v = tile[swz(L)];
+                                float2 wv;
+                                if (xo == 0) {
+                                    wv = tile[swz(L ^ xl)];
+                                } else {  // partner amplitude in another tile (read-only pass only)
+                                    wv = st[(base + pdep64(L, P.tile_mask)) ^ oxm];
+                                }
+                                const double cr = (double)wv.x * v.x + (double)wv.y * v.y;
+                                const double ci = (double)wv.x * v.y - (double)wv.y * v.x;
+                                double t;
+                                switch (ony & 3) {
+                                    case 0: t = cr; break;
+                                    case 1: t = -ci; break;
+                                    case 2: t = -cr; break;
+                                    default: t = ci; break;
+                                }
+                                const int par = (__popc(L & zl) + zs) & 1;
+                                part[0] += par ? -t : t;
+                            }
                         }
-                        bar_wg(wg);
+                        // warp sums parked per (observable, warp); one barrier pair per 16
+                        // strings, then a fixed-order sum over the 8 warps
+#pragma unroll
+                        for (int sh = 16; sh > 0; sh >>= 1) part[0] += __shfl_xor_sync(0xffffffffu, part[0], sh);
+                        double* park = red + 128;  // 16 strings x 8 warps
+                        const int jo = o & 15;
+                        if (lane == 0) park[jo * NWW + (wtid >> 5)] = part[0];
+                        if (jo == 15 || o + 1 == P.obs_count) {
+                            bar_wg(wg);
+                            // column of string o - jo + lane of this chunk
+                            const int sl = __shfl_sync(0xffffffffu, cslot, (j - jo + lane) & 31);
+                            if (wtid <= jo) {
+                                double v = 0.0;
+#pragma unroll
+                                for (int w2 = 0; w2 < NWW; ++w2) v += park[wtid * NWW + w2];
+                                A.obs_part[tile_row * A.n_obs + sl] = v;
+                            }
+                            bar_wg(wg);
+                        }
                     }
                 }
             }

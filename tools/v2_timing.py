@@ -16,7 +16,13 @@ runpy.run_path(sys.argv[0], run_name="__main__")
 buf = (ctypes.c_ulonglong * 16)()
 qtraj.lib().qt_v2_timing_read(buf)
 names = ["item start -> tile ready (desc, bases, full wait)", "gather", "MMA complete wait", "write back",
-         "epilogues", "stores + end barrier", "next loads", "W wait + MMA issue", "L/X transition"]
-tot = sum(buf[i] for i in range(9))
+         "observables epilogue", "stores + end barrier", "next loads", "W wait + MMA issue", "L/X transition",
+         "rho epilogue", "final blocksum epilogue"]
+tot = sum(buf[i] for i in range(11))
+items = max(buf[11], 1)
 for i, nm in enumerate(names):
-    print(f"  {nm:50s} {buf[i]:14d} cyc  {100.0 * buf[i] / max(tot, 1):5.1f}%")
+    print(f"  {nm:50s} {buf[i]:14d} cyc  {100.0 * buf[i] / max(tot, 1):5.1f}%  {buf[i] / items:9.0f} cyc/item")
+print(f"  items {buf[11]}  tensor-core gates {buf[12]}  gathers {buf[13]}  rho items {buf[14]}  final items {buf[15]}")
+print(f"  per item: {tot / items:.0f} cyc; per gate (MMA + transition phases): "
+      f"{(buf[2] + buf[7] + buf[8]) / max(buf[12], 1):.0f} cyc; per rho item {buf[9] / max(buf[14], 1):.0f} cyc; "
+      f"per gather {buf[1] / max(buf[13], 1):.0f} cyc")
