@@ -78,14 +78,17 @@ constexpr int kGateShiftBit = 16;         // bits 16..23: run scale headroom (lo
 //   (TMEM lane bits 0..4, warp bits 0..1), [13..18] = xu (next-gate source columns).
 constexpr int32_t kGateV2 = 0x800;
 #ifdef __CUDACC__
-#define QT_HD __host__ __device__
+#define QT_DESC_HD __host__ __device__
 #else
-#define QT_HD
+#define QT_DESC_HD
 #endif
-QT_HD inline uint16_t* v2_units(GateDesc& g) { return reinterpret_cast<uint16_t*>(&g.rpos); }
-QT_HD inline const uint16_t* v2_units(const GateDesc& g) { return reinterpret_cast<const uint16_t*>(&g.rpos); }
+QT_DESC_HD inline uint16_t* v2_units(GateDesc& g) { return reinterpret_cast<uint16_t*>(&g.rpos); }
+QT_DESC_HD inline const uint16_t* v2_units(const GateDesc& g) { return reinterpret_cast<const uint16_t*>(&g.rpos); }
 constexpr int32_t kGateRunEnd = 0x1000;
 constexpr int32_t kGateXNext = 0x2000;  // v2: the transition to the next gate is an X (16x256b) transposition
+// v2: matrix bit 0 is tile bit 0, so configurations c, c ^ 1 are one 16-byte pair of
+// the fp32 tile (gather / write-back by 16-byte shared-memory accesses)
+constexpr int32_t kGatePair0 = 0x4000;
 // Pool bytes of a v2 gate operand: B = 32 rows x [W_hi (32 f16) | W_lo (32 f16)], SWIZZLE_128B.
 constexpr int kV2GateBytes = 4096;
 // Pool bytes of a tensor-core gate operand padded to k qubits (tc_common.cuh

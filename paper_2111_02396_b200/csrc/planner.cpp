@@ -581,6 +581,26 @@ void v2_layouts(GateDesc* gd, const uint32_t* lmask, const double* norms, int co
         if (first >= 0) cfg[m++] = first;
         for (int t = 0; t < nr; ++t) cfg[m++] = rest[t];
     };
+    // tile bit 0 as matrix bit 0 (16-byte pair gathers / write-backs, kGatePair0) when
+    // it is one of the two bits leaving at the next X transition anyway
+    auto pair0 = [](V2Lay& L) {
+        if (L.cfg[1] == 0) std::swap(L.cfg[0], L.cfg[1]);
+    };
+    // modelled shared-memory wavefronts per 8 bytes of a warp's fp32-tile access with
+    // this layout (2 = conflict-free): 16-byte pair accesses are served per quarter warp
+    // (lane bits 0..2 must reach 8 distinct 16-byte chunks), 8-byte ones per half warp
+    // (lane bits 0..3 must reach the 16 bank pairs)
+    auto wf8 = [](const V2Lay& L) {
+        const int nl = L.cfg[0] == 0 ? 3 : 4;
+        unsigned basis[4];
+        int r = 0;
+        for (int t = 0; t < nl; ++t) {
+            unsigned v = v2_bank(L.lane[t]);
+            for (int j = 0; j < r; ++j) v = std::min(v, v ^ basis[j]);
+            if (v) basis[r++] = v;
+        }
+        return 2 << (nl - r);
+    };
     // fresh layout of gate i (segment start: gathered from the fp32 tile)
     auto fresh = [&](int i, V2Lay& L) {
         order_cfg(i, -1, L.cfg);
@@ -598,8 +618,35 @@ void v2_layouts(GateDesc* gd, const uint32_t* lmask, const double* norms, int co
         for (int t = 0; t < 5; ++t) L.lane[lane_order[t]] = fut[2 + t];
         L.warp[0] = fut[7];
         L.warp[1] = fut[8];
-        // bank-conflict-free gathers want tile bit 0 in lane bit 0 when it is a lane
-        // bit at all (the other low lane bits keep their arrival order)
+        pair0(L);
+        // conflict-free gathers: swap lane bits 0..2 with the warp bits (the tile bits
+        // needed last) when that lowers the modelled wavefronts, lane bit 0 first
+        int best = wf8(L);
+        V2Lay B = L;
+        static const int lpos[3] = {0, 2, 1};
+        for (int a = 0; a < 3 && best > 2; ++a)
+            for (int w = 0; w < 2; ++w) {
+                V2Lay X = L;
+                std::swap(X.lane[lpos[a]], X.warp[w]);
+                const int f = wf8(X);
+                if (f < best) {
+                    best = f;
+                    B = X;
+                }
+            }
+        for (int a = 0; a < 3 && best > 2; ++a)
+            for (int b = a + 1; b < 3; ++b)
+                for (int w = 0; w < 2; ++w) {
+                    V2Lay X = L;
+                    std::swap(X.lane[lpos[a]], X.warp[w]);
+                    std::swap(X.lane[lpos[b]], X.warp[1 - w]);
+                    const int f = wf8(X);
+                    if (f < best) {
+                        best = f;
+                        B = X;
+                    }
+                }
+        L = B;
     };
     auto local_of = [](const V2Lay& L) {
         uint32_t m = 0;
@@ -628,6 +675,7 @@ void v2_layouts(GateDesc* gd, const uint32_t* lmask, const double* norms, int co
                 t = 1;  // L: same rows, new roles of the 6 thread-local bits
                 V2Lay& L = lay[i];
                 order_cfg(i, -1, L.cfg);
+                pair0(L);
                 int g2[6], ng2 = 0;
                 for (int b = 0; b < T; ++b)
                     if (((local & ~lmask[i]) >> b) & 1u) g2[ng2++] = b;
@@ -672,7 +720,7 @@ void v2_layouts(GateDesc* gd, const uint32_t* lmask, const double* norms, int co
         const V2Lay& L = lay[i];
         const bool start = tr[i] == 0;
         const bool end = i + 1 >= count || !(gd[i + 1].k & kGateTC) || tr[i + 1] == 0;
-        int32_t k = (gd[i].k & ~(kGateRunStart | kGateRunEnd | kGateXNext | (0xff << kGateShiftBit))) | kGateV2;
+        int32_t k = (gd[i].k & ~(kGateRunStart | kGateRunEnd | kGateXNext | kGatePair0 | (0xff << kGateShiftBit))) | kGateV2;
         if (start) {
             double c = 1.0;
             for (int j = i; j < count && (gd[j].k & kGateTC) && (j == i || tr[j] != 0); ++j) c *= norms[j];
@@ -681,6 +729,7 @@ void v2_layouts(GateDesc* gd, const uint32_t* lmask, const double* norms, int co
         }
         if (end) k |= kGateRunEnd;
         if (!end && tr[i + 1] == 2) k |= kGateXNext;
+        if (L.cfg[0] == 0) k |= kGatePair0;
         uint16_t u[20] = {0};
         for (int r = 0; r < 4; ++r) u[r] = unit((uint32_t)L.cfg[r]);
         for (int r = 0; r < 2; ++r) u[4 + r] = unit((uint32_t)L.grp[r]);

@@ -1107,7 +1107,7 @@ extern "C" qt_status qt_plan_bank_stats(qt_plan plan, uint64_t seed, uint64_t tr
 
 // Diagnostic (undeclared, like qt_plan_bank_stats): the pass / fused-gate structure of
 // one trajectory's program.  out = [n_pass, then per pass: tile_mask, flags,
-// gate_count, then per gate: global qubit mask of its (padded) matrix bits, k].
+// gate_count, then per gate: global qubit mask of its (padded) matrix bits, k, 5 words of v2 units].
 extern "C" qt_status qt_plan_dump(qt_plan plan, uint64_t seed, uint64_t traj, int64_t* out, int64_t cap) {
     if (!plan || !out) return fail(QT_EINVAL, "NULL argument");
     const Plan& P = plan_of(plan);
@@ -1138,6 +1138,14 @@ extern "C" qt_status qt_plan_dump(qt_plan plan, uint64_t seed, uint64_t traj, in
             }
             put((int64_t)m);
             put(G.k);
+            // v2 layout units (20 x uint16, desc.hpp v2_units), zeros for other kernels
+            uint16_t u[20] = {0};
+            if (G.k & kGateV2) std::memcpy(u, v2_units(G), sizeof u);
+            for (int j = 0; j < 5; ++j) {
+                int64_t x = 0;
+                std::memcpy(&x, u + 4 * j, 8);
+                put(x);
+            }
         }
     }
     return w <= cap ? QT_OK : fail(QT_EINVAL, "plan dump: capacity too small");

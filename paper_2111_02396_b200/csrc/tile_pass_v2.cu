@@ -568,6 +568,8 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                     else if (k == 2) apply_fused<2, 5>(tile, M, swz(tb) << 3, unit);
                     else apply_fused<3, 5>(tile, M, swz(tb) << 3, unit);
                     bar_wg(wg);
+                    QT_T(16);
+                    QT_C(17, 1);
                     ++g;
                     continue;
                 }
@@ -576,15 +578,29 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                     const Fp32Layout L = fp32_layout(gds[g], wtid);
                     uint64_t v[32];
                     float amax = 0.f;
+                    if (gds[g].k & kGatePair0) {
+                        // matrix bit 0 = tile bit 0: configurations c, c + 1 are one 16-byte pair
 #pragma unroll
-                    for (int jj = 0; jj < 2; ++jj)
+                        for (int jj = 0; jj < 2; ++jj)
 #pragma unroll
-                        for (int c = 0; c < 16; ++c) {
-                            const uint32_t o = (jj ? L.base1 : L.base0) ^ L.c01[c & 3] ^ L.c23[c >> 2];
-                            const float2 f = *reinterpret_cast<const float2*>(tb8 + o);
-                            v[16 * jj + c] = pk2(f.x, f.y);
-                            amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
-                        }
+                            for (int c = 0; c < 16; c += 2) {
+                                const uint32_t o = (jj ? L.base1 : L.base0) ^ L.c01[c & 3] ^ L.c23[c >> 2];
+                                const float4 f = *reinterpret_cast<const float4*>(tb8 + o);
+                                v[16 * jj + c] = pk2(f.x, f.y);
+                                v[16 * jj + c + 1] = pk2(f.z, f.w);
+                                amax = fmaxf(amax, fmaxf(fmaxf(fabsf(f.x), fabsf(f.y)), fmaxf(fabsf(f.z), fabsf(f.w))));
+                            }
+                    } else {
+#pragma unroll
+                        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+                            for (int c = 0; c < 16; ++c) {
+                                const uint32_t o = (jj ? L.base1 : L.base0) ^ L.c01[c & 3] ^ L.c23[c >> 2];
+                                const float2 f = *reinterpret_cast<const float2*>(tb8 + o);
+                                v[16 * jj + c] = pk2(f.x, f.y);
+                                amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
+                            }
+                    }
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
                     float* redf = reinterpret_cast<float*>(red);
@@ -653,17 +669,30 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                         // ---- segment end: D -> fp32 tile ----
                         const Fp32Layout L = fp32_layout(gds[g], wtid);
                         const uint64_t inv2 = pk2(run_inv, run_inv);
+                        const bool pair = (gk & kGatePair0) != 0;
 #pragma unroll
                         for (int jj = 0; jj < 2; ++jj) {
                             uint32_t d[32];
                             tc::tmem_ld32(tlh + 64u * (uint32_t)jj, d);
                             tc::tmem_wait_ld();
                             const uint32_t o0 = jj ? L.base1 : L.base0;
+                            if (pair) {
 #pragma unroll
-                            for (int c = 0; c < 16; ++c) {
-                                const uint32_t o = o0 ^ L.c01[c & 3] ^ L.c23[c >> 2];
-                                *reinterpret_cast<float2*>(tb8 + o) = upk2(
-                                    mul2(pk2(__uint_as_float(d[2 * c]), __uint_as_float(d[2 * c + 1])), inv2));
+                                for (int c = 0; c < 16; c += 2) {
+                                    const uint32_t o = o0 ^ L.c01[c & 3] ^ L.c23[c >> 2];
+                                    const float2 a = upk2(
+                                        mul2(pk2(__uint_as_float(d[2 * c]), __uint_as_float(d[2 * c + 1])), inv2));
+                                    const float2 b = upk2(
+                                        mul2(pk2(__uint_as_float(d[2 * c + 2]), __uint_as_float(d[2 * c + 3])), inv2));
+                                    *reinterpret_cast<float4*>(tb8 + o) = make_float4(a.x, a.y, b.x, b.y);
+                                }
+                            } else {
+#pragma unroll
+                                for (int c = 0; c < 16; ++c) {
+                                    const uint32_t o = o0 ^ L.c01[c & 3] ^ L.c23[c >> 2];
+                                    *reinterpret_cast<float2*>(tb8 + o) = upk2(
+                                        mul2(pk2(__uint_as_float(d[2 * c]), __uint_as_float(d[2 * c + 1])), inv2));
+                                }
                             }
                         }
                         tc::fence_before();
@@ -794,7 +823,9 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                 QT_T(10);
                 QT_C(15, 1);
             }
+            QT_T(18);
             if (P.flags & kPassObs) {
+                QT_C(19, 1);
                 // Z strings: Walsh-Hadamard transform of |psi(wtid + m NT)|^2 over m
                 float w[NA];
 #pragma unroll
@@ -811,19 +842,50 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                             w[m] = a + c;
                             w[m | h] = a - c;
                         }
-                // observable descriptors: lane l of every warp holds string o0 + l of the
-                // chunk, broadcast by shuffles (no dependent global load per string)
-                for (int o0 = 0; o0 < P.obs_count; o0 += 32) {
+                // observable descriptors: lane l < 16 of every warp holds string o0 + l of
+                // the chunk, broadcast by shuffles (no dependent global load per string)
+                for (int o0 = 0; o0 < P.obs_count; o0 += 16) {
                     uint64_t cx = 0, cz = 0;
                     int cny = 0, cslot = 0;
-                    if (o0 + lane < P.obs_count) {
+                    if (lane < 16 && o0 + lane < P.obs_count) {
                         const ObsDesc& Ol = A.obs[P.obs_begin + o0 + lane];
                         cx = Ol.xmask;
                         cz = Ol.zmask;
                         cny = Ol.ny;
                         cslot = Ol.slot;
                     }
-                    const int oc = min(32, P.obs_count - o0);
+                    const int oc = min(16, P.obs_count - o0);
+                    if (__all_sync(0xffffffffu, cx == 0)) {
+                        // Z strings only: the 16 thread partials side by side, one warp
+                        // reduce-scatter, one fixed-order sum over the 8 warps
+                        double pv[16];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const uint64_t ozm = __shfl_sync(0xffffffffu, cz, j);
+                            pv[j] = 0.0;
+                            if (j < oc) {
+                                const uint32_t zl = P.tile_mask == (uint64_t)(TILE - 1) ? (uint32_t)(ozm & (TILE - 1))
+                                                                                         : to_local<T>(ozm, P);
+                                const int zs = __popcll(base & ozm) & 1;
+                                const float vv = pick_uniform<NA>(w, (int)(zl >> 8));
+                                const int par = (__popc((uint32_t)wtid & zl & (uint32_t)(NT - 1)) + zs) & 1;
+                                pv[j] = par ? -(double)vv : (double)vv;
+                            }
+                        }
+                        const double r = warp_reduce_scatter<16>(pv, lane);
+                        double* park = red + 128;  // 8 warps x 16 strings
+                        bar_wg(wg);
+                        if ((lane & 1) == 0) park[(wtid >> 5) * 16 + (lane >> 1)] = r;
+                        bar_wg(wg);
+                        if (wtid < oc) {
+                            double v = 0.0;
+#pragma unroll
+                            for (int w2 = 0; w2 < NWW; ++w2) v += park[w2 * 16 + wtid];
+                            A.obs_part[tile_row * A.n_obs + cslot] = v;  // lane wtid holds string o0 + wtid
+                        }
+                        continue;
+                    }
+                    bar_wg(wg);  // park's readers of a previous chunk are done
                     for (int j = 0; j < oc; ++j) {
                         const int o = o0 + j;
                         const uint64_t oxm = __shfl_sync(0xffffffffu, cx, j);
@@ -875,7 +937,7 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                         if (jo == 15 || o + 1 == P.obs_count) {
                             bar_wg(wg);
                             // column of string o - jo + lane of this chunk
-                            const int sl = __shfl_sync(0xffffffffu, cslot, (j - jo + lane) & 31);
+                            const int sl = __shfl_sync(0xffffffffu, cslot, (j - jo + lane) & 15);
                             if (wtid <= jo) {
                                 double v = 0.0;
 #pragma unroll
@@ -926,10 +988,10 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
 size_t tile_pass_v2_smem_bytes() { return v2::kSmemBytes; }
 #ifdef QT_V2_TIMING
 static unsigned long long* g_v2_tbuf = nullptr;
-// diagnostics build: clock64 phase sums of warpgroup leaders of CTA 7 (16 counters)
+// diagnostics build: clock64 phase sums of warpgroup leaders of CTA 7 (32 counters)
 extern "C" void qt_v2_timing_read(unsigned long long* out) {
     cudaDeviceSynchronize();
-    if (g_v2_tbuf) cudaMemcpy(out, g_v2_tbuf, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    if (g_v2_tbuf) cudaMemcpy(out, g_v2_tbuf, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
 }
 #endif
 
@@ -952,8 +1014,8 @@ cudaError_t launch_tile_pass_v2(const TileArgs& a, int step, uint32_t ntiles, in
     const uint32_t grid = nitems < (uint32_t)sms ? nitems : (uint32_t)sms;
 #ifdef QT_V2_TIMING
     if (!g_v2_tbuf) {
-        cudaMalloc(&g_v2_tbuf, 16 * sizeof(unsigned long long));
-        cudaMemset(g_v2_tbuf, 0, 16 * sizeof(unsigned long long));
+        cudaMalloc(&g_v2_tbuf, 32 * sizeof(unsigned long long));
+        cudaMemset(g_v2_tbuf, 0, 32 * sizeof(unsigned long long));
     }
     TileArgs b2 = a;
     b2.timing = g_v2_tbuf;

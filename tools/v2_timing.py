@@ -13,15 +13,20 @@ from paper_2111_02396_b200 import qtraj  # noqa: E402
 qtraj.LIB_PATH = qtraj.LIB_PATH.replace("libqtraj.so", "libqtraj_v2t.so")
 sys.argv = [sys.argv[1]] + sys.argv[2:]
 runpy.run_path(sys.argv[0], run_name="__main__")
-buf = (ctypes.c_ulonglong * 16)()
+buf = (ctypes.c_ulonglong * 32)()
 qtraj.lib().qt_v2_timing_read(buf)
-names = ["item start -> tile ready (desc, bases, full wait)", "gather", "MMA complete wait", "write back",
+names = ["tile full wait", "gather", "MMA complete wait", "write back",
          "observables epilogue", "stores + end barrier", "next loads", "W wait + MMA issue", "L/X transition",
          "rho epilogue", "final blocksum epilogue"]
-tot = sum(buf[i] for i in range(11))
+names += [""] * 5 + ["CUDA-core gates (device-chosen operators)", "", "before the observables epilogue", "",
+                      "item start barrier", "first W copies issued"]
+tot = sum(buf[i] for i in range(11)) + buf[16] + buf[18] + buf[20] + buf[21]
 items = max(buf[11], 1)
 for i, nm in enumerate(names):
+    if not nm:
+        continue
     print(f"  {nm:50s} {buf[i]:14d} cyc  {100.0 * buf[i] / max(tot, 1):5.1f}%  {buf[i] / items:9.0f} cyc/item")
+print(f"  CUDA-core gates {buf[17]}  observable items {buf[19]}")
 print(f"  items {buf[11]}  tensor-core gates {buf[12]}  gathers {buf[13]}  rho items {buf[14]}  final items {buf[15]}")
 print(f"  per item: {tot / items:.0f} cyc; per gate (MMA + transition phases): "
       f"{(buf[2] + buf[7] + buf[8]) / max(buf[12], 1):.0f} cyc; per rho item {buf[9] / max(buf[14], 1):.0f} cyc; "
