@@ -14,6 +14,7 @@
 //  4. Epilogues: rho_Q at each barrier; block sums (+ Pauli partials) at the
 //     end of the trajectory.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 
@@ -553,6 +554,7 @@ void v2_layouts(GateDesc* gd, const uint32_t* lmask, const double* norms, int co
                 std::vector<ConsDesc>& cons, const int* gate_fused) {
     constexpr int T = 13;
     constexpr int kNever = 1 << 20;
+    static const bool half_split = getenv("QT_V2_HALF") && atoi(getenv("QT_V2_HALF")) != 0;
     auto bits_of = [](uint32_t m, int* out) {
         int k = 0;
         for (int b = 0; b < 13; ++b)
@@ -612,12 +614,22 @@ void v2_layouts(GateDesc* gd, const uint32_t* lmask, const double* norms, int co
         // group bits: the two needed soonest (local transitions); then lane bits by
         // arrival through X transitions (L3, L4 next, L1, L2 after one X, L0 after
         // two); the bits never needed are warp bits
-        L.grp[0] = fut[0];
-        L.grp[1] = fut[1];
         static const int lane_order[5] = {3, 4, 1, 2, 0};
-        for (int t = 0; t < 5; ++t) L.lane[lane_order[t]] = fut[2 + t];
-        L.warp[0] = fut[7];
-        L.warp[1] = fut[8];
+        if (half_split) {
+            // group bit 1 selects the warpgroup half and stays for the whole segment:
+            // with the warp bits it takes the three bits needed last
+            L.grp[0] = fut[0];
+            for (int t = 0; t < 5; ++t) L.lane[lane_order[t]] = fut[1 + t];
+            L.warp[0] = fut[6];
+            L.warp[1] = fut[7];
+            L.grp[1] = fut[8];
+        } else {
+            L.grp[0] = fut[0];
+            L.grp[1] = fut[1];
+            for (int t = 0; t < 5; ++t) L.lane[lane_order[t]] = fut[2 + t];
+            L.warp[0] = fut[7];
+            L.warp[1] = fut[8];
+        }
         pair0(L);
         // conflict-free gathers: swap lane bits 0..2 with the warp bits (the tile bits
         // needed last) when that lowers the modelled wavefronts, lane bit 0 first
@@ -670,7 +682,7 @@ void v2_layouts(GateDesc* gd, const uint32_t* lmask, const double* norms, int co
         int t = 0;
         if (prev_tc && cum * norms[i] <= 16.0) {
             const V2Lay& P = lay[i - 1];
-            const uint32_t local = local_of(P);
+            const uint32_t local = local_of(P) & ~(half_split ? (1u << P.grp[1]) : 0u);
             if ((lmask[i] & ~local) == 0) {
                 t = 1;  // L: same rows, new roles of the 6 thread-local bits
                 V2Lay& L = lay[i];
@@ -680,13 +692,13 @@ void v2_layouts(GateDesc* gd, const uint32_t* lmask, const double* norms, int co
                 for (int b = 0; b < T; ++b)
                     if (((local & ~lmask[i]) >> b) & 1u) g2[ng2++] = b;
                 L.grp[0] = g2[0];
-                L.grp[1] = g2[1];
+                L.grp[1] = half_split ? P.grp[1] : g2[1];
                 std::memcpy(L.lane, P.lane, sizeof L.lane);
                 std::memcpy(L.warp, P.warp, sizeof L.warp);
             } else {
                 // X: rows (c0, c1, L0, L1, L2 | warps); local = {L3, L4, c2, c3, j0, j1}
                 const uint32_t lx = (1u << P.lane[3]) | (1u << P.lane[4]) | (1u << P.cfg[2]) | (1u << P.cfg[3]) |
-                                    (1u << P.grp[0]) | (1u << P.grp[1]);
+                                    (1u << P.grp[0]) | (half_split ? 0u : (1u << P.grp[1]));
                 if ((lmask[i] & ~lx) == 0 && ((lmask[i] >> P.lane[3]) & 1u)) {
                     t = 2;
                     V2Lay& L = lay[i];
@@ -695,7 +707,7 @@ void v2_layouts(GateDesc* gd, const uint32_t* lmask, const double* norms, int co
                     for (int b = 0; b < T; ++b)
                         if (((lx & ~lmask[i]) >> b) & 1u) g2[ng2++] = b;
                     L.grp[0] = g2[0];
-                    L.grp[1] = g2[1];
+                    L.grp[1] = half_split ? P.grp[1] : g2[1];
                     L.lane[0] = P.cfg[0];
                     L.lane[1] = P.cfg[1];
                     L.lane[2] = P.lane[0];

@@ -30,6 +30,17 @@ constexpr int T = 13;
 constexpr int TILE = 1 << T;
 constexpr uint32_t kTileBytes = TILE * 8;  // 64 KB
 constexpr int NBUF = 3;
+// W operands by one 4 KB bulk copy (async proxy, no proxy fence before the MMAs) instead
+// of 16-byte cp.async from every thread (whose consumer fence waits for the issuing
+// thread's outstanding tile loads)
+#ifndef QT_V2_BULKW
+#define QT_V2_BULKW 1
+#endif
+// L2 prefetch of the tile an item loads when done, at the item's context preparation
+// (measured slower on C2: 9380 -> 9069 traj/s; kept off)
+#ifndef QT_V2_L2PF
+#define QT_V2_L2PF 0
+#endif
 constexpr int NWG = 2;
 constexpr int NT = 256;        // threads per compute warpgroup: 2 warps per TMEM lane quarter
 constexpr int NWW = NT / 32;   // warps per warpgroup
@@ -389,8 +400,8 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
         for (int b = 0; b < NBUF; ++b) mbar_init_s(full_bar(b), NT);
         for (int w = 0; w < NWG; ++w) {
             mbar_init_s(mma_bar(w), 4);  // one commit per issuing warp
-            mbar_init_s(wfull_bar(w, 0), NT);
-            mbar_init_s(wfull_bar(w, 1), NT);
+            mbar_init_s(wfull_bar(w, 0), QT_V2_BULKW ? 1 : NT);
+            mbar_init_s(wfull_bar(w, 1), QT_V2_BULKW ? 1 : NT);
         }
         tc::fence_mbar_init();
     }
@@ -479,12 +490,60 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
             const int nch = c->p.gate_count * (int)(sizeof(GateDesc) / 16);
             for (int k = lane; k < nch; k += 32) cp_async16_s(dst + 16u * (uint32_t)k, src + k);
             asm volatile("cp.async.commit_group;\n" ::: "memory");
+#if QT_V2_L2PF
+            // the tile this item loads when done (ordinal jj + 3, about two items ahead):
+            // its 512 runs of 128 B into L2, so the cp.async load later hits L2
+            if (i3 < nitems && !(c->p3.flags & kPassInit)) {
+                __syncwarp();
+                const PassDesc& P3 = c->p3;
+                uint64_t ofix = 0;
+#pragma unroll
+                for (int q = 0; q < 5; ++q) ofix |= (uint64_t)((lane >> q) & 1) << P3.tq[4 + q];
+                const float2* s3 = A.state + ((uint64_t)P3.slot << A.n) + c->base3 + ofix;
+                const uint64_t e0 = 1ull << P3.tq[9], e1 = 1ull << P3.tq[10], e2 = 1ull << P3.tq[11],
+                               e3 = 1ull << P3.tq[12];
+#pragma unroll
+                for (uint32_t k = 0; k < 16; ++k) {
+                    const uint64_t x = ((k & 1) ? e0 : 0ull) + ((k & 2) ? e1 : 0ull) + ((k & 4) ? e2 : 0ull) +
+                                       ((k & 8) ? e3 : 0ull);
+                    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(s3 + x));
+                }
+            }
+#endif
         };
         // prologue: the first item's context, then the first loads (ordinals 0 and 2 by
         // warpgroup 0, ordinal 1 by warpgroup 1)
+        // W operands (4 KB per tensor-core gate, two buffers per warpgroup): every thread
+        // copies 16 bytes with cp.async (1-D bulk copies were measured an order of
+        // magnitude slower, profiles/r2_ubench_stream.txt).  cp.async.mbarrier.arrive
+        // tracks ALL earlier cp.async of the thread, so an item's first two operands are
+        // issued at the end of the warpgroup's previous item, before its tile load;
+        // later ones as soon as a buffer's MMAs complete.
+        auto issue_w_of = [&](const GateDesc* gl, int ngl, int& wn) {
+            while (wn < ngl && !(gl[wn].k & kGateTC)) ++wn;
+            if (wn < ngl) {
+                const uint32_t wi = w_issued & 1u;
+#if QT_V2_BULKW
+                if (wtid == 32) bulk_w(wbuf + wi * kV2GateBytes, A.pool + gl[wn].mat_off, wfull_bar(wg, (int)wi));
+#else
+                cp_async16_s(wbuf + wi * kV2GateBytes + 16u * (uint32_t)wtid,
+                             reinterpret_cast<const char*>(A.pool + gl[wn].mat_off) + 16 * wtid);
+                cp_async_arrive_noinc(wfull_bar(wg, (int)wi));
+#endif
+                ++w_issued;
+                ++wn;
+            }
+        };
+        int w_carry = 0;  // operands of this warpgroup's next item already issued
         if (prep_warp) {
             prep_a(wg);
             prep_b(wg, &ctxs[0]);
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        bar_wg(wg);
+        if (raw(wg) < nitems) {
+            issue_w_of(ctxs[0].g, ctxs[0].p.gate_count, w_carry);
+            issue_w_of(ctxs[0].g, ctxs[0].p.gate_count, w_carry);
         }
         for (int jj = 0; jj < NBUF; ++jj) {
             const uint32_t i = raw(jj);
@@ -513,9 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
             const uint32_t i = raw(jj);
             const uint32_t i3 = raw(jj + NBUF);  // loaded into b by this warpgroup when done
             const int b = jj % NBUF;
-            Ctx* cx = &ctxs[kk & 1];
-            if (prep_warp) asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // this item's gate descriptors
-            bar_wg(wg);  // context visible; the previous item's readers of the other context are done
+            Ctx* cx = &ctxs[kk & 1];  // complete and visible since the previous item's end
             if (prep_warp) prep_a(jj + 2);
             bool prep_pending = prep_warp;
             const PassDesc& P = cx->p;
@@ -526,24 +583,8 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
             float2* tile = reinterpret_cast<float2*>(sm + (size_t)b * kTileBytes);
             char* const tb8 = reinterpret_cast<char*>(tile);
             const int ng = P.gate_count;
-            // W (bulk copies, two buffers): the first two tensor-core gates' operands travel
-            // with the tile; later ones are issued as soon as a buffer's MMAs complete
-            int w_next = 0;  // next gate whose W has not been issued
-            // (every thread copies 16 bytes with cp.async; 1-D bulk copies were measured an
-            // order of magnitude slower, profiles/r2_ubench_stream.txt)
-            auto issue_w = [&]() {
-                while (w_next < ng && !(gds[w_next].k & kGateTC)) ++w_next;
-                if (w_next < ng) {
-                    const uint32_t wi = w_issued & 1u;
-                    cp_async16_s(wbuf + wi * kV2GateBytes + 16u * (uint32_t)wtid,
-                                 reinterpret_cast<const char*>(A.pool + gds[w_next].mat_off) + 16 * wtid);
-                    cp_async_arrive_noinc(wfull_bar(wg, (int)wi));
-                    ++w_issued;
-                    ++w_next;
-                }
-            };
-            issue_w();
-            issue_w();
+            int w_next = w_carry;  // next gate whose W has not been issued
+            auto issue_w = [&]() { issue_w_of(gds, ng, w_next); };
             const uint64_t base = cx->base, base3 = cx->base3;
             // every thread acquires the tile's "full" phase (the cp.async writes of the
             // loading warpgroup; a single poller + bar.sync would order them too, but
@@ -635,7 +676,10 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                         // threads (lane 0 of warps 0..3) keep the tensor pipe fed
                         const uint32_t wi = w_used & 1u;
                         mbar_wait_s(wfull_bar(wg, (int)wi), (w_used >> 1) & 1u);
+                        QT_T(22);
+#if !QT_V2_BULKW
                         tc::fence_proxy_async();  // cp.async (generic proxy) writes -> tensor-core reads
+#endif
                         tc::fence_after();
                         const uint32_t wb = wbuf + wi * kV2GateBytes;
                         const uint64_t b0 = tc::smem_desc_sw128(wb), b1 = tc::smem_desc_sw128(wb + 32);
@@ -970,8 +1014,15 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                     *reinterpret_cast<float4*>(((m & 1) ? d1 : dst) + x) = v;
                 }
             }
-            bar_wg(wg);  // every read of the buffer and of the staged descriptors done
+            if (prep_warp) asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // next item's context
+            bar_wg(wg);  // every read of the buffer and of the staged descriptors done; next context visible
             QT_T(5);
+            w_carry = 0;
+            if (raw(jj + 2) < nitems) {
+                const Ctx* nx = &ctxs[(kk + 1) & 1];
+                issue_w_of(nx->g, nx->p.gate_count, w_carry);
+                issue_w_of(nx->g, nx->p.gate_count, w_carry);
+            }
             if (i3 < nitems) load_item(jj + NBUF, cx->p3, i3 & ((1u << tshift) - 1u), base3, wtid);
             asm volatile("cp.async.commit_group;\n" ::: "memory");
             QT_T(6);

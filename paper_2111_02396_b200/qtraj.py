@@ -14,7 +14,7 @@ from typing import Iterable, List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqtraj.so")
+LIB_PATH = os.environ.get("QT_LIB_PATH") or os.path.join(_HERE, "libqtraj.so")  # QT_LIB_PATH: experiment builds
 
 STATUS = {0: "QT_OK", -1: "QT_EINVAL", -2: "QT_EQUBIT", -3: "QT_EARITY", -4: "QT_ENONUNITARY",
           -5: "QT_ENONCPTP", -6: "QT_EOOM", -7: "QT_ECUDA", -8: "QT_ENCCL", -9: "QT_ELEAK",

@@ -16,11 +16,11 @@ runpy.run_path(sys.argv[0], run_name="__main__")
 buf = (ctypes.c_ulonglong * 32)()
 qtraj.lib().qt_v2_timing_read(buf)
 names = ["tile full wait", "gather", "MMA complete wait", "write back",
-         "observables epilogue", "stores + end barrier", "next loads", "W wait + MMA issue", "L/X transition",
+         "observables epilogue", "stores + end barrier", "next loads", "MMA issue (after W)", "L/X transition",
          "rho epilogue", "final blocksum epilogue"]
 names += [""] * 5 + ["CUDA-core gates (device-chosen operators)", "", "before the observables epilogue", "",
-                      "item start barrier", "first W copies issued"]
-tot = sum(buf[i] for i in range(11)) + buf[16] + buf[18] + buf[20] + buf[21]
+                      "item start barrier", "first W copies issued", "W operand wait (issuer)"]
+tot = sum(buf[i] for i in range(11)) + buf[16] + buf[18] + buf[20] + buf[21] + buf[22]
 items = max(buf[11], 1)
 for i, nm in enumerate(names):
     if not nm:
