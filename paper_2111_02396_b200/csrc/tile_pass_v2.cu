@@ -109,6 +109,27 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint3
                  "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
                  "r"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+// One group's gate GEMM, D = x_hi W_hi + x_lo W_hi + x_hi W_lo: six M128 N32 K16 MMAs
+// (A = [x_hi | x_lo] at TMEM columns ah .. ah + 31, B = W rows at 32-byte K offsets of
+// the SW128 descriptor b0) and the commit, in one asm block: the derived operands are
+// formed inside it, so ptxas moves d / ah / b0 into uniform registers once.
+__device__ __forceinline__ void mma6_commit(uint32_t d, uint32_t ah, uint64_t b0, uint32_t mbar) {
+    constexpr uint32_t idesc = tc::idesc_f16_m128(32);
+    asm volatile(
+        "{\n\t.reg .pred p0, p1;\n\t.reg .b32 a1, a2, a3;\n\t.reg .b64 b1, b2, b3;\n\t"
+        "setp.ne.b32 p0, 0, 0;\n\tsetp.eq.b32 p1, 0, 0;\n\t"
+        "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+        "add.u64 b1, %2, 2;\n\tadd.u64 b2, %2, 4;\n\tadd.u64 b3, %2, 6;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, p1;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], %2, %3, p1;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b1, %3, p1;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], b2, %3, p1;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b3, %3, p1;\n\t"
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n\t}\n" ::"r"(d),
+        "r"(ah), "l"(b0), "r"(idesc), "r"(mbar)
+        : "memory");
+}
 __device__ __forceinline__ void tmem_ld2(uint32_t taddr, uint32_t& a, uint32_t& b) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];\n" : "=r"(a), "=r"(b) : "r"(taddr) : "memory");
 }
@@ -682,16 +703,8 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
 #endif
                         tc::fence_after();
                         const uint32_t wb = wbuf + wi * kV2GateBytes;
-                        const uint64_t b0 = tc::smem_desc_sw128(wb), b1 = tc::smem_desc_sw128(wb + 32);
-                        const uint64_t b2 = tc::smem_desc_sw128(wb + 64), b3 = tc::smem_desc_sw128(wb + 96);
-                        const uint32_t d = tbase + 64u * (uint32_t)(wtid >> 5), ah = d + 32u, al = d + 48u;
-                        mma_ts(d, ah, b0, 0u);
-                        mma_ts(d, ah + 8u, b1, 1u);
-                        mma_ts(d, al, b0, 1u);
-                        mma_ts(d, al + 8u, b1, 1u);
-                        mma_ts(d, ah, b2, 1u);
-                        mma_ts(d, ah + 8u, b3, 1u);
-                        tc::mma_commit(reinterpret_cast<uint64_t*>(sm + kMbarOff + 8 * (6 + wg)));
+                        const uint32_t d = tbase + 64u * (uint32_t)(wtid >> 5);
+                        mma6_commit(d, d + 32u, tc::smem_desc_sw128(wb), mma_bar(wg));
                         QT_T(7);
                     }
                     ++w_used;
