@@ -133,6 +133,7 @@ struct FuseItem {
     bool fixed;  // never merged (device-chosen conventional op)
 };
 // Returns fused gates as lists of item indices (time order inside each).
-std::vector<std::vector<int>> fuse_items(const std::vector<FuseItem>& items, int f);
+// Two-phase fuser: fused gate j = items flat[offs[j] .. offs[j + 1]) in time order.
+void fuse_items(const FuseItem* items, int N, int f, std::vector<int>& flat, std::vector<int>& offs);
 
 }  // namespace qt

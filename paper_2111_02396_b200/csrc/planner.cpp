@@ -14,6 +14,7 @@
 //  4. Epilogues: rho_Q at each barrier; block sums (+ Pauli partials) at the
 //     end of the trajectory.
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -26,30 +27,83 @@ namespace qt {
 static inline int popc(uint64_t x) { return __builtin_popcountll(x); }
 
 // ---------------------------------------------------------------------------
-// Two-phase fuser.
+// Two-phase fuser.  Flat arrays in a per-thread scratch (planning runs
+// per trajectory on every host thread; no heap traffic in steady state).
 // ---------------------------------------------------------------------------
-std::vector<std::vector<int>> fuse_items(const std::vector<FuseItem>& items, int f) {
-    const int N = (int)items.size();
-    std::vector<std::vector<int>> out;
-    if (N == 0) return out;
-    int nq_max = 0;
-    for (auto& it : items) nq_max = std::max(nq_max, 64 - __builtin_clzll(it.mask | 1));
-    // per-qubit item sequences
-    std::vector<std::vector<int>> on_q(nq_max);
-    std::vector<std::array<int, 6>> slot(N);  // position of item in each of its qubits' lists
+namespace {
+struct FuseScratch {
+    std::vector<int> qcnt, qoff, onq, slot;         // per-qubit item lists (CSR), item slots (6 per item)
+    std::vector<int> group, gid, anchor;            // phase 1 groups
+    std::vector<char> absorbed, has_members;
+    std::vector<int> moff, mem;                     // members per group (CSR, time order)
+    std::vector<uint64_t> gmask;
+    std::vector<char> gfixed, marked;
+    std::vector<int> gqcnt, gqoff, gq, gpos;        // per-qubit group lists (CSR), group slots (6 per group)
+    std::vector<int> F, last;                       // phase 2 growth
+};
+template <class V>
+inline void fit(V& v, size_t n) {
+    if (v.size() < n) v.resize(n);
+}
+}  // namespace
+
+#ifdef QT_PLAN_PROFILE
+// diagnostics build: seconds spent per planning phase (single-threaded callers)
+static double g_prof[8];
+extern "C" void qt_plan_profile(double* o) {
+    for (int i = 0; i < 8; ++i) o[i] = g_prof[i];
+}
+#define QT_PP(k)                                                                                      \
+    do {                                                                                              \
+        const auto t_now = std::chrono::steady_clock::now();                                          \
+        g_prof[k] += std::chrono::duration<double>(t_now - t_pp).count();                             \
+        t_pp = t_now;                                                                                 \
+    } while (0)
+#else
+#define QT_PP(k)
+#endif
+
+void fuse_items(const FuseItem* items, int N, int f, std::vector<int>& flat, std::vector<int>& offs) {
+#ifdef QT_PLAN_PROFILE
+    auto t_pp = std::chrono::steady_clock::now();
+#endif
+    flat.clear();
+    offs.assign(1, 0);
+    if (N == 0) return;
+    thread_local FuseScratch S;
+    int nq = 0;
+    for (int i = 0; i < N; ++i) nq = std::max(nq, 64 - __builtin_clzll(items[i].mask | 1));
+    // per-qubit item sequences (CSR) and each item's slot in them
+    fit(S.qcnt, nq);
+    fit(S.qoff, nq + 1);
+    std::fill(S.qcnt.begin(), S.qcnt.begin() + nq, 0);
+    for (int i = 0; i < N; ++i)
+        for (uint64_t mk = items[i].mask; mk; mk &= mk - 1) ++S.qcnt[__builtin_ctzll(mk)];
+    S.qoff[0] = 0;
+    for (int q = 0; q < nq; ++q) S.qoff[q + 1] = S.qoff[q] + S.qcnt[q];
+    fit(S.onq, S.qoff[nq]);
+    fit(S.slot, 6 * (size_t)N);
+    std::fill(S.qcnt.begin(), S.qcnt.begin() + nq, 0);
     for (int i = 0; i < N; ++i) {
         int m = 0;
-        for (uint64_t mk = items[i].mask; mk; mk &= mk - 1) {
+        for (uint64_t mk = items[i].mask; mk; mk &= mk - 1, ++m) {
             const int q = __builtin_ctzll(mk);
-            slot[i][m++] = (int)on_q[q].size();
-            on_q[q].push_back(i);
+            S.slot[6 * i + m] = S.qcnt[q];
+            S.onq[S.qoff[q] + S.qcnt[q]++] = i;
         }
     }
+    auto onq = [&](int q, int k) { return S.onq[S.qoff[q] + k]; };
     // ---- phase 1: absorb small items into time-adjacent larger ones on the same qubits
-    std::vector<int> group(N);
-    for (int i = 0; i < N; ++i) group[i] = i;
-    auto k_of = [&](int g) { return popc(items[g].mask); };
-    std::vector<char> absorbed(N, 0);
+    fit(S.group, N);
+    fit(S.absorbed, N);
+    fit(S.has_members, N);
+    int* group = S.group.data();
+    for (int i = 0; i < N; ++i) {
+        group[i] = i;
+        S.absorbed[i] = 0;
+        S.has_members[i] = 0;
+    }
+    auto kq = [&](int g) { return popc(items[g].mask); };
     // forward absorption (an item joins the next larger item on all of its qubits); reverse order
     for (int i = N - 1; i >= 0; --i) {
         if (items[i].fixed) continue;
@@ -58,176 +112,188 @@ std::vector<std::vector<int>> fuse_items(const std::vector<FuseItem>& items, int
         int m = 0;
         for (uint64_t mk = items[i].mask; mk && ok; mk &= mk - 1, ++m) {
             const int q = __builtin_ctzll(mk);
-            const int pos = slot[i][m];
-            if (pos + 1 >= (int)on_q[q].size()) { ok = false; break; }
-            const int g = group[on_q[q][pos + 1]];
+            const int pos = S.slot[6 * i + m];
+            if (pos + 1 >= S.qcnt[q]) { ok = false; break; }
+            const int g = group[onq(q, pos + 1)];
             if (G < 0) G = g;
             else if (G != g) ok = false;
         }
         if (!ok || G < 0 || items[G].fixed) continue;
-        if (!((items[i].mask & ~items[G].mask) == 0 && popc(items[i].mask) < k_of(G))) continue;
+        if (!((items[i].mask & ~items[G].mask) == 0 && popc(items[i].mask) < kq(G))) continue;
         group[i] = G;
-        absorbed[i] = 1;
+        S.absorbed[i] = 1;
     }
     // backward absorption of trailing small items into the previous larger item
-    std::vector<char> has_members(N, 0);
     for (int i = 0; i < N; ++i)
-        if (group[i] != i) has_members[group[i]] = 1;
+        if (group[i] != i) S.has_members[group[i]] = 1;
     for (int i = 0; i < N; ++i) {
-        if (items[i].fixed || absorbed[i] || has_members[i]) continue;
+        if (items[i].fixed || S.absorbed[i] || S.has_members[i]) continue;
         int G = -1;
         bool ok = true;
         int m = 0;
         for (uint64_t mk = items[i].mask; mk && ok; mk &= mk - 1, ++m) {
             const int q = __builtin_ctzll(mk);
-            const int pos = slot[i][m];
+            const int pos = S.slot[6 * i + m];
             if (pos == 0) { ok = false; break; }
-            const int g = group[on_q[q][pos - 1]];
+            const int g = group[onq(q, pos - 1)];
             if (G < 0) G = g;
             else if (G != g) ok = false;
         }
         if (!ok || G < 0 || items[G].fixed) continue;
-        if (!((items[i].mask & ~items[G].mask) == 0 && popc(items[i].mask) < k_of(G))) continue;
+        if (!((items[i].mask & ~items[G].mask) == 0 && popc(items[i].mask) < kq(G))) continue;
         group[i] = G;
-        absorbed[i] = 1;
-        has_members[G] = 1;
+        S.absorbed[i] = 1;
+        S.has_members[G] = 1;
     }
-    // groups: anchor id -> members (time order)
-    std::vector<int> gid(N, -1);
-    std::vector<std::vector<int>> members;
-    std::vector<uint64_t> gmask;
-    std::vector<char> gfixed;
-    for (int i = 0; i < N; ++i) {
-        const int a = group[i];
-        if (gid[a] < 0) {
-            gid[a] = (int)members.size();
-            members.emplace_back();
-            gmask.push_back(items[a].mask);
-            gfixed.push_back(items[a].fixed);
-        }
-    }
-    for (int i = 0; i < N; ++i) members[gid[group[i]]].push_back(i);
-    const int NG = (int)members.size();
-    // group order = anchor order (gid assigned in anchor order of first appearance);
-    // re-sort by anchor index to be safe
-    std::vector<int> anchor_of(NG);
+    QT_PP(6);
+    // groups in anchor order (rank = group id); members in time order
+    fit(S.gid, N);
+    int G = 0;
     for (int i = 0; i < N; ++i)
-        if (group[i] == i) anchor_of[gid[i]] = i;
-    std::vector<int> gorder(NG);
-    for (int g = 0; g < NG; ++g) gorder[g] = g;
-    std::sort(gorder.begin(), gorder.end(), [&](int a, int b) { return anchor_of[a] < anchor_of[b]; });
-    std::vector<int> grank(NG);
-    for (int r = 0; r < NG; ++r) grank[gorder[r]] = r;
-    // per-qubit group sequences (dedup consecutive), verify they follow rank order
-    std::vector<std::vector<int>> gq(nq_max);
-    bool valid = true;
-    for (int q = 0; q < nq_max; ++q) {
-        for (int it : on_q[q]) {
-            const int g = gid[group[it]];
-            if (gq[q].empty() || gq[q].back() != g) {
-                // strictly increasing rank also rules out non-contiguous groups
-                if (!gq[q].empty() && grank[gq[q].back()] >= grank[g]) valid = false;
-                gq[q].push_back(g);
+        if (group[i] == i) S.gid[i] = G++;
+    fit(S.gmask, N);
+    fit(S.gfixed, N);
+    fit(S.moff, N + 1);
+    fit(S.mem, N);
+    auto build_groups = [&](bool phase1) {
+        if (!phase1) {
+            G = N;
+            for (int i = 0; i < N; ++i) S.gid[i] = i;
+        }
+        std::fill(S.moff.begin(), S.moff.begin() + G + 1, 0);
+        for (int i = 0; i < N; ++i) {
+            const int a = phase1 ? group[i] : i;
+            ++S.moff[S.gid[a] + 1];
+            if (a == i) {
+                S.gmask[S.gid[i]] = items[i].mask;
+                S.gfixed[S.gid[i]] = items[i].fixed;
             }
         }
-    }
-    if (!valid) {
-        // fall back: no phase-1 absorption
-        members.assign(N, {});
-        gmask.resize(N);
-        gfixed.resize(N);
-        for (int i = 0; i < N; ++i) {
-            members[i] = {i};
-            gmask[i] = items[i].mask;
-            gfixed[i] = items[i].fixed;
+        for (int g = 0; g < G; ++g) S.moff[g + 1] += S.moff[g];
+        fit(S.last, G);
+        for (int g = 0; g < G; ++g) S.last[g] = S.moff[g];
+        for (int i = 0; i < N; ++i) S.mem[S.last[S.gid[phase1 ? group[i] : i]]++] = i;
+        // per-qubit group sequences (dedup consecutive); valid iff strictly increasing rank
+        fit(S.gqcnt, nq);
+        fit(S.gqoff, nq + 1);
+        fit(S.gq, S.qoff[nq]);
+        bool valid = true;
+        for (int q = 0; q < nq; ++q) {
+            int c = 0;
+            const int base = S.qoff[q];
+            for (int k = 0; k < S.qcnt[q]; ++k) {
+                const int g = S.gid[phase1 ? group[onq(q, k)] : onq(q, k)];
+                if (c == 0 || S.gq[base + c - 1] != g) {
+                    if (c > 0 && S.gq[base + c - 1] >= g) valid = false;
+                    S.gq[base + c++] = g;
+                }
+            }
+            S.gqcnt[q] = c;
+            S.gqoff[q] = base;
         }
-        gorder.resize(N);
-        grank.resize(N);
-        for (int i = 0; i < N; ++i) gorder[i] = grank[i] = i;
-        for (int q = 0; q < nq_max; ++q) gq[q] = on_q[q];
-    }
-    const int G = (int)members.size();
+        return valid;
+    };
+    if (!build_groups(true)) build_groups(false);  // fall back: no phase-1 absorption
     // position of each group in each of its qubits' group lists
-    std::vector<std::array<int, 6>> gpos(G);
-    for (int q = 0; q < nq_max; ++q)
-        for (int k = 0; k < (int)gq[q].size(); ++k) {
-            const int g = gq[q][k];
+    fit(S.gpos, 6 * (size_t)G);
+    for (int q = 0; q < nq; ++q)
+        for (int k = 0; k < S.gqcnt[q]; ++k) {
+            const int g = S.gq[S.gqoff[q] + k];
             int m = 0;
-            for (uint64_t mk = gmask[g]; mk; mk &= mk - 1, ++m)
-                if (__builtin_ctzll(mk) == q) gpos[g][m] = k;
+            for (uint64_t mk = S.gmask[g]; mk; mk &= mk - 1, ++m)
+                if (__builtin_ctzll(mk) == q) S.gpos[6 * g + m] = k;
         }
     auto pos_on = [&](int g, int q) {
         int m = 0;
-        for (uint64_t mk = gmask[g]; mk; mk &= mk - 1, ++m)
-            if (__builtin_ctzll(mk) == q) return gpos[g][m];
+        for (uint64_t mk = S.gmask[g]; mk; mk &= mk - 1, ++m)
+            if (__builtin_ctzll(mk) == q) return S.gpos[6 * g + m];
         return -1;
     };
+    auto gqat = [&](int q, int k) { return S.gq[S.gqoff[q] + k]; };
+    QT_PP(7);
     // ---- phase 2: greedy growth in increasing time order
-    std::vector<char> marked(G, 0);
+    fit(S.marked, G);
+    std::fill(S.marked.begin(), S.marked.begin() + G, 0);
+    char* marked = S.marked.data();
     auto ready = [&](int h) {  // all predecessors of h marked
-        for (uint64_t mk = gmask[h]; mk; mk &= mk - 1) {
+        int m = 0;
+        for (uint64_t mk = S.gmask[h]; mk; mk &= mk - 1, ++m) {
             const int q = __builtin_ctzll(mk);
-            const int p = pos_on(h, q);
-            if (p > 0 && !marked[gq[q][p - 1]]) return false;
+            const int p = S.gpos[6 * h + m];
+            if (p > 0 && !marked[gqat(q, p - 1)]) return false;
         }
         return true;
     };
-    for (int r = 0; r < G; ++r) {
-        const int g0 = gorder[r];
+    fit(S.last, (size_t)std::max(nq, 1));
+    flat.reserve(N);
+    offs.reserve(G + 1);
+    for (int g0 = 0; g0 < G; ++g0) {
         if (marked[g0]) continue;
-        std::vector<int> F{g0};
+        S.F.clear();
+        S.F.push_back(g0);
         marked[g0] = 1;
-        uint64_t FM = gmask[g0];
-        if (!gfixed[g0]) {
+        uint64_t FM = S.gmask[g0];
+        // last[q]: latest position of a member of F on qubit q (q in FM)
+        {
+            int m = 0;
+            for (uint64_t mk = FM; mk; mk &= mk - 1, ++m) S.last[__builtin_ctzll(mk)] = S.gpos[6 * g0 + m];
+        }
+        uint64_t cur = FM;  // qubits whose last[] is set
+        auto add_group = [&](int g) {
+            marked[g] = 1;
+            S.F.push_back(g);
+            int m = 0;
+            for (uint64_t mk = S.gmask[g]; mk; mk &= mk - 1, ++m) {
+                const int q = __builtin_ctzll(mk);
+                const int p = S.gpos[6 * g + m];
+                if (!((cur >> q) & 1) || p > S.last[q]) S.last[q] = p;
+            }
+            cur |= S.gmask[g];
+        };
+        if (!S.gfixed[g0]) {
             bool added = true;
             while (added) {
                 added = false;
                 for (uint64_t mk = FM; mk; mk &= mk - 1) {
                     const int q = __builtin_ctzll(mk);
-                    // latest member of F on q, then the next group on q
-                    int last = -1;
-                    for (int g : F) {
-                        if (gmask[g] >> q & 1) last = std::max(last, pos_on(g, q));
-                    }
-                    if (last < 0 || last + 1 >= (int)gq[q].size()) continue;
-                    const int h = gq[q][last + 1];
-                    if (marked[h] || gfixed[h]) continue;
+                    // the next group on q after F's latest member there
+                    const int lq = S.last[q];
+                    if (lq + 1 >= S.gqcnt[q]) continue;
+                    const int h = gqat(q, lq + 1);
+                    if (marked[h] || S.gfixed[h]) continue;
                     // unmarked predecessors of h (next-nearest neighbours back in time)
-                    std::vector<int> preds;
+                    int preds[6], np = 0;
                     bool ok = true;
-                    uint64_t nm = FM | gmask[h];
-                    for (uint64_t hm = gmask[h]; hm && ok; hm &= hm - 1) {
+                    uint64_t nm = FM | S.gmask[h];
+                    int m = 0;
+                    for (uint64_t hm = S.gmask[h]; hm && ok; hm &= hm - 1, ++m) {
                         const int p = __builtin_ctzll(hm);
-                        const int ph = pos_on(h, p);
+                        const int ph = S.gpos[6 * h + m];
                         if (ph <= 0) continue;
-                        const int pg = gq[p][ph - 1];
+                        const int pg = gqat(p, ph - 1);
                         if (marked[pg]) continue;
-                        if (gfixed[pg] || !ready(pg)) { ok = false; break; }
-                        if (std::find(preds.begin(), preds.end(), pg) == preds.end()) {
-                            preds.push_back(pg);
-                            nm |= gmask[pg];
+                        if (S.gfixed[pg] || !ready(pg)) { ok = false; break; }
+                        bool seen = false;
+                        for (int j = 0; j < np; ++j) seen |= preds[j] == pg;
+                        if (!seen) {
+                            preds[np++] = pg;
+                            nm |= S.gmask[pg];
                         }
                     }
                     if (!ok || popc(nm) > f) continue;
-                    for (int pg : preds) {
-                        marked[pg] = 1;
-                        F.push_back(pg);
-                    }
-                    marked[h] = 1;
-                    F.push_back(h);
+                    for (int j = 0; j < np; ++j) add_group(preds[j]);
+                    add_group(h);
                     FM = nm;
                     added = true;
                     break;  // restart from the lowest qubit with the grown set
                 }
             }
         }
-        std::sort(F.begin(), F.end(), [&](int a, int b) { return grank[a] < grank[b]; });
-        std::vector<int> fused_items;
-        for (int g : F)
-            for (int it : members[g]) fused_items.push_back(it);
-        out.push_back(std::move(fused_items));
+        std::sort(S.F.begin(), S.F.end());
+        for (int g : S.F)
+            for (int k = S.moff[g]; k < S.moff[g + 1]; ++k) flat.push_back(S.mem[k]);
+        offs.push_back((int)flat.size());
     }
-    return out;
 }
 
 // ---------------------------------------------------------------------------
@@ -237,8 +303,11 @@ namespace {
 
 struct FusedGate {
     uint64_t mask;
-    std::vector<int> items;  // indices into the segment item list
-    int special_event;       // >= 0: device-chosen conventional op (no materialization)
+    const int* items;  // indices into the segment item list (the fuser's flat output)
+    int n_items;
+    int special_event;  // >= 0: device-chosen conventional op (no materialization)
+    const int* begin() const { return items; }
+    const int* end() const { return items + n_items; }
 };
 
 struct Item {
@@ -561,14 +630,21 @@ void v2_layouts(GateDesc* gd, const uint32_t* lmask, const double* norms, int co
             if ((m >> b) & 1u) out[k++] = b;
         return k;
     };
-    // first gate index > i that uses tile bit b (tensor-core gates of this pass)
-    auto next_use = [&](int i, int b) {
-        for (int j = i + 1; j < count; ++j) {
-            if (!(gd[j].k & kGateTC)) break;
-            if ((lmask[j] >> b) & 1u) return j;
+    // first gate index > i that uses tile bit b (tensor-core gates of this pass), from a
+    // table filled by one backward scan
+    thread_local std::vector<int> nu_tab;
+    if (nu_tab.size() < (size_t)13 * (count + 1)) nu_tab.resize((size_t)13 * (count + 1));
+    for (int b = 0; b < 13; ++b) nu_tab[(size_t)13 * count + b] = kNever;
+    for (int j = count - 1; j >= 0; --j)
+        for (int b = 0; b < 13; ++b) {
+            // entry j: next use after gate j - 1 ... stored as "first index >= j"
+            int v;
+            if (!(gd[j].k & kGateTC)) v = kNever;
+            else if ((lmask[j] >> b) & 1u) v = j;
+            else v = nu_tab[(size_t)13 * (j + 1) + b];
+            nu_tab[(size_t)13 * j + b] = v;
         }
-        return kNever;
-    };
+    auto next_use = [&](int i, int b) { return nu_tab[(size_t)13 * (i + 1) + b]; };
     // matrix-bit order of gate i's qubits: `first` (or -1) fixed at bit 0, then the
     // qubits needed latest at bits 0 / 1 (they leave for lane bits at an X transition),
     // the ones needed soonest at bits 2 / 3
@@ -804,20 +880,42 @@ void v2_layouts(GateDesc* gd, const uint32_t* lmask, const double* norms, int co
 
 qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const ObsGroups& og,
                           TrajProgram& out, int mode) {
-    out = TrajProgram();
+#ifdef QT_PLAN_PROFILE
+    auto t_pp = std::chrono::steady_clock::now();
+#endif
+    // reset, keeping the vectors' capacity (callers reuse programs across batches)
+    out.passes.clear();
+    out.gates.clear();
+    out.fused.clear();
+    out.cons.clear();
+    out.events.clear();
+    out.records.clear();
+    out.pool_size = 0;
+    out.n_deferred = out.n_conventional = 0;
+    out.alg_bytes = out.alg_flops = 0;
     const bool conventional = (mode == 1);  // no lower bounds, every channel reduces
     const int n = P.n;
     const int T = P.T;
     out.records.assign(P.n_recorded, -1);
     // ---- 1. draws + Alg. 2 first loop; build segments
-    std::vector<std::vector<Item>> segs(1);
+    // per-thread scratch, reused across trajectories
+    thread_local std::vector<std::vector<Item>> segs;
+    thread_local size_t nsegs;
+    nsegs = 1;
+    if (segs.empty()) segs.emplace_back();
+    segs[0].clear();
+    auto new_seg = [&]() {
+        if (segs.size() <= nsegs) segs.emplace_back();
+        segs[nsegs++].clear();
+    };
     struct Barrier { int event; uint64_t qmask; };
-    std::vector<Barrier> barriers;
+    thread_local std::vector<Barrier> barriers;
+    barriers.clear();
     for (const PlanOp& op : P.ops) {
         if (op.kind == 0) {
             // sweep gates (P:262 parametrized circuits): variant = parameter set traj mod n_sets
             const int v = op.var_base + (op.n_kraus > 1 ? (int)(traj % (uint64_t)P.n_sets) : 0);
-            if (!P.vars[v].identity) segs.back().push_back(Item{op.mask, v, -1, op.nq});
+            if (!P.vars[v].identity) segs[nsegs - 1].push_back(Item{op.mask, v, -1, op.nq});
             continue;
         }
         const double u = draw(seed, (uint32_t)op.chan, kPurposeChannel, traj, 0);
@@ -834,7 +932,7 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
             ++out.n_deferred;
             if (op.record >= 0) out.records[op.record] = pick;
             const int v = op.var_base + pick;
-            if (!P.vars[v].identity) segs.back().push_back(Item{op.mask, v, -1, op.nq});
+            if (!P.vars[v].identity) segs[nsegs - 1].push_back(Item{op.mask, v, -1, op.nq});
             continue;
         }
         // conventional: barrier + device-chosen op opening the next segment
@@ -850,45 +948,56 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
         const int ev = (int)out.events.size();
         out.events.push_back(E);
         barriers.push_back(Barrier{ev, op.mask});
-        segs.emplace_back();
-        segs.back().push_back(Item{op.mask, -1, ev, op.nq});
+        new_seg();
+        segs[nsegs - 1].push_back(Item{op.mask, -1, ev, op.nq});
     }
+    QT_PP(0);
     // ---- 2.+3. fuse each segment, pack passes
     const uint64_t lowS = low_mask(std::min(P.CL, n));
     const uint64_t lowT = low_mask(T);
     int32_t pool = 0;
-    std::vector<uint64_t> gate_masks;  // parallel to out.gates
-    std::vector<double> gate_norms;    // parallel to out.gates: spectral-norm bound
-    std::vector<int> gate_fused;       // parallel to out.gates: FusedDesc index or -1
+    thread_local std::vector<uint64_t> gate_masks;  // parallel to out.gates
+    thread_local std::vector<double> gate_norms;    // parallel to out.gates: spectral-norm bound
+    thread_local std::vector<int> gate_fused;       // parallel to out.gates: FusedDesc index or -1
+    gate_masks.clear();
+    gate_norms.clear();
+    gate_fused.clear();
     auto alloc = [&](int d2) {
         const int32_t off = pool;
         pool += (d2 + 1) & ~1;  // keep 16-byte alignment
         return off;
     };
-    for (size_t si = 0; si < segs.size(); ++si) {
+    for (size_t si = 0; si < nsegs; ++si) {
         const std::vector<Item>& items = segs[si];
-        std::vector<FuseItem> fi(items.size());
+        thread_local std::vector<FuseItem> fi;
+        thread_local std::vector<int> fflat, foffs;
+        fi.resize(items.size());
         for (size_t i = 0; i < items.size(); ++i) fi[i] = FuseItem{items[i].mask, items[i].var < 0};
-        std::vector<std::vector<int>> groups = fuse_items(fi, P.f);
-        std::vector<FusedGate> fg;
-        fg.reserve(groups.size());
-        for (auto& g : groups) {
+        QT_PP(1);
+        fuse_items(fi.data(), (int)fi.size(), P.f, fflat, foffs);
+        QT_PP(2);
+        thread_local std::vector<FusedGate> fg;
+        fg.clear();
+        for (size_t gi = 0; gi + 1 < foffs.size(); ++gi) {
             FusedGate x;
+            x.items = fflat.data() + foffs[gi];
+            x.n_items = foffs[gi + 1] - foffs[gi];
             x.mask = 0;
             x.special_event = -1;
-            for (int it : g) x.mask |= items[it].mask;
-            if (g.size() == 1 && items[g[0]].var < 0) x.special_event = items[g[0]].event;
+            for (int it : x) x.mask |= items[it].mask;
+            if (x.n_items == 1 && items[x.items[0]].var < 0) x.special_event = items[x.items[0]].event;
             if (x.special_event < 0)
-                for (int it : g)
+                for (int it : x)
                     if (items[it].var < 0) return QT_EINVAL;  // fixed item fused (cannot happen)
-            x.items = std::move(g);
-            fg.push_back(std::move(x));
+            fg.push_back(x);
         }
         // pass packing
-        std::vector<char> taken(fg.size(), 0);
+        thread_local std::vector<char> taken;
+        taken.assign(fg.size(), 0);
         size_t remaining = fg.size();
-        const bool last_seg = (si + 1 == segs.size());
-        std::vector<size_t> seg_pass_idx;
+        const bool last_seg = (si + 1 == nsegs);
+        thread_local std::vector<size_t> seg_pass_idx;
+        seg_pass_idx.clear();
         // tensor cores: a fused gate is padded to tc_k qubits with the lowest
         // qubits it does not touch, which must lie in the tile too
         auto padded = [&](const FusedGate& g) {
@@ -900,7 +1009,8 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
         while (remaining > 0) {
             uint64_t S = lowS;
             uint64_t blocked = 0;
-            std::vector<int> chosen;
+            thread_local std::vector<int> chosen;
+            chosen.clear();
             for (size_t i = 0; i < fg.size(); ++i) {
                 if (taken[i]) continue;
                 const uint64_t gm = fg[i].mask;
@@ -931,7 +1041,7 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
                 gd.k = popc(g.mask);
                 gd.rpos = gd.tpos = 0;  // after S is final
                 double gnorm = 1.0;
-                for (int it : g.items)
+                for (int it : g)
                     if (items[it].var >= 0) gnorm *= P.vars[items[it].var].norm;
                 if (g.special_event >= 0) {
                     const int d = 1 << gd.k;
@@ -947,8 +1057,8 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
                     fd.mat_off = gd.mat_off;
                     fd.k = popc(pm) | (P.tc ? kGateTC : 0) | (P.v2 ? kGateV2 : 0);
                     fd.cons_begin = (int32_t)out.cons.size();
-                    fd.cons_count = (int32_t)g.items.size();
-                    for (int it : g.items) {
+                    fd.cons_count = (int32_t)g.n_items;
+                    for (int it : g) {
                         ConsDesc c;
                         c.var = items[it].var;
                         uint32_t pos = 0;
@@ -976,6 +1086,7 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
             seg_pass_idx.push_back(out.passes.size());
             out.passes.push_back(pd);
         }
+        QT_PP(3);
         // barrier epilogue: rho_Q of the next conventional channel
         if (!last_seg) {
             const Barrier& b = barriers[si];
@@ -1016,7 +1127,8 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
                 gate_layout(gate_masks[pd.gate_begin + g], pd.tile_mask, T, R, gd.rpos, gd.tpos);
             }
             if (P.v2) {
-                std::vector<uint32_t> lm(pd.gate_count);
+                thread_local std::vector<uint32_t> lm;
+                lm.resize(pd.gate_count);
                 for (int g = 0; g < pd.gate_count; ++g) {
                     uint32_t l = 0;
                     int i = 0;
@@ -1034,6 +1146,7 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
             }
         }
     }
+    QT_PP(4);
     // ---- 4. final epilogue: block sums over the low T qubits (+ observables of
     // group 0), then read-only passes for the other observable groups
     if (og.final_pass) {
@@ -1075,6 +1188,7 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
         pd.slot = 0;
     }
     out.pool_size = pool;
+    QT_PP(5);
     // algorithmic bytes: 2^(n+4) per storing pass, 2^(n+3) per read-only pass
     for (auto& pd : out.passes) out.alg_bytes += std::ldexp(1.0, n + ((pd.flags & kPassStore) ? 4 : 3));
     return QT_OK;

@@ -641,7 +641,7 @@ qt_status qt_run_trajectories(qt_ctx ctx, qt_plan plan, const qt_run_opts* opts,
     qt_status status = QT_OK;
     for (uint64_t j0 = 0; j0 < opts->traj_count && status == QT_OK; j0 += (uint64_t)batch) {
         const int ns = (int)std::min<uint64_t>((uint64_t)batch, opts->traj_count - j0);
-        progs.assign(ns, TrajProgram());
+        progs.resize(ns);  // plan_trajectory resets a program keeping its capacity
         trajs.resize(ns);
         for (int b = 0; b < ns; ++b) trajs[b] = opts->traj_begin + (j0 + b) * stride;
         std::vector<qt_status> pst(ns, QT_OK);
@@ -873,6 +873,25 @@ qt_status qt_plan_info(qt_plan plan, uint64_t seed, uint64_t traj, int64_t* out)
     out[7] = (int64_t)pg.cons.size();
     out[8] = P.T;
     out[9] = P.v2 ? 13 : (P.tc ? P.tc_k : 0);
+    return QT_OK;
+}
+
+// Diagnostic (undeclared): host planning cost -- plans trajectories traj0 .. traj0 + count - 1
+// on one thread into one reused program (as the runtime's per-slot programs are reused)
+// and returns the seconds spent.
+extern "C" qt_status qt_plan_bench(qt_plan plan, uint64_t seed, uint64_t traj0, int count, double* seconds) {
+    if (!plan || !seconds || count < 0) return fail(QT_EINVAL, "bad argument");
+    const Plan& P = plan_of(plan);
+    ObsGroups og;
+    og.ranges.push_back({0, 0});
+    og.masks.push_back(0);
+    TrajProgram pg;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int j = 0; j < count; ++j) {
+        const qt_status e = plan_trajectory(P, seed, traj0 + (uint64_t)j, og, pg);
+        if (e != QT_OK) return e;
+    }
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return QT_OK;
 }
 

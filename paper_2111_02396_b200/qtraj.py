@@ -249,6 +249,14 @@ class Plan:
                 "tile_bits", "kernel"]
         return dict(zip(keys, list(out)))
 
+    def plan_seconds(self, seed: int, traj0: int, count: int) -> float:
+        """Host planning cost (diagnostic qt_plan_bench): seconds to plan trajectories
+        traj0 .. traj0 + count - 1 on one thread into one reused program."""
+        sec = ctypes.c_double()
+        _check(lib().qt_plan_bench(self.h, ctypes.c_uint64(seed), ctypes.c_uint64(traj0), int(count),
+                                   ctypes.byref(sec)))
+        return sec.value
+
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:
             _lib.qt_plan_destroy(self.h)
