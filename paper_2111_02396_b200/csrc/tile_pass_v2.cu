@@ -38,6 +38,11 @@ constexpr int NBUF = 3;
 #endif
 // L2 prefetch of the tile an item loads when done, at the item's context preparation
 // (measured slower on C2: 9380 -> 9069 traj/s; kept off)
+// MMA completion: every thread polls the commit mbarrier (1) or one thread polls and a
+// warpgroup barrier releases the others (0)
+#ifndef QT_V2_ALLWAIT
+#define QT_V2_ALLWAIT 1
+#endif
 #ifndef QT_V2_L2PF
 #define QT_V2_L2PF 0
 #endif
@@ -715,9 +720,15 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                         prep_b(jj + 2, &ctxs[(kk + 1) & 1]);
                         prep_pending = false;
                     }
+#if QT_V2_ALLWAIT
+                    // every thread acquires the MMAs' completion itself (no barrier round trip)
+                    while (!mbar_try(mma_bar(wg), mma_phase)) {
+                    }
+#else
                     if (elect) mbar_wait_s(mma_bar(wg), mma_phase);
                     tc::fence_before();
                     bar_wg(wg);
+#endif
                     QT_T(2);
                     mma_phase ^= 1u;
                     tc::fence_after();
