@@ -53,6 +53,11 @@ static void canonicalize(int nq, const int* qubits, const double* in, int* q_sor
         }
 }
 
+// canonical form of operation i (sorted qubits, internal matrix order)
+const HostOp* circuit_op(const qt_circuit_s* c, int i) {
+    return (c && i >= 0 && i < (int)c->c.ops.size()) ? &c->c.ops[i] : nullptr;
+}
+
 static double max_dev_from_identity_of_gram(int d, const cd* const* mats, int count) {
     // || sum_i M_i^dag M_i - I ||_max
     double worst = 0.0;

@@ -10,6 +10,7 @@
 
 #include "../../include/qtraj.h"
 #include "desc.hpp"
+#include <cuda_runtime_api.h>
 
 namespace qt {
 
@@ -30,6 +31,11 @@ struct HostOp {
     int record = 0;
     std::vector<cd> mats;  // n_kraus * d * d (internal order)
 };
+
+const HostOp* circuit_op(const qt_circuit_s* c, int i);
+// streaming single-gate pass (gate_stream.cu); cudaErrorNotSupported if n < 7 + max(nq, 4)
+cudaError_t gate_stream_apply(cudaStream_t s, void* state, int n, int nq, const int* qs, const cd* U, int repeats,
+                              double* kernel_ms);
 
 struct Circuit {
     int n = 0;

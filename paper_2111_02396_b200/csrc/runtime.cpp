@@ -833,6 +833,19 @@ qt_status qt_apply_gate_ex(qt_ctx ctx, void* state_dev, int n, int nq, const int
         qt_circuit_destroy(c);
         return e;
     }
+    // the streaming single-gate kernel (TMA tiles, tensor cores) when the register holds
+    // its tiles; QT_GATE_STREAM=0 selects the trajectory kernels for A/B runs
+    static const bool stream_off = getenv("QT_GATE_STREAM") && atoi(getenv("QT_GATE_STREAM")) == 0;
+    if (!stream_off) {
+        const HostOp* op = circuit_op(c, 0);
+        cudaError_t ce = gate_stream_apply(ctx->stream, state_dev, n, op->nq, op->q, op->mats.data(), repeats, kernel_ms);
+        if (ce != cudaErrorNotSupported) {
+            qt_circuit_destroy(c);
+            if (ce != cudaSuccess) return fail(QT_ECUDA, std::string("gate_stream: ") + cudaGetErrorString(ce));
+            return QT_OK;
+        }
+        cudaGetLastError();
+    }
     qt_fuse_opts o{};
     o.max_fused = std::max(nq, 2);
     // one fused gate per HBM pass: the per-tile kernel (12-qubit tiles) streams these faster
