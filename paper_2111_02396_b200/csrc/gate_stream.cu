@@ -481,60 +481,83 @@ static bool plan_gate(void* state, int n, int nq, const int* qs, const cd* U, Gs
         if (!((mmask >> q) & 1)) rowq.push_back(q);
     const int T = L + (int)high.size();
     if (T != 7 + K || n < T || n - L > 31) return false;
-    // tile bit of each matrix bit
-    int tpos[6];
-    for (int m = 0, h = 0; m < K; ++m) tpos[m] = mq[m] < L ? mq[m] : L + h++;
     GsArgs& a = P.a;
     a.L = L;
     a.tile_mask = ((1ull << L) - 1ull);
     for (int h : high) a.tile_mask |= 1ull << h;
     a.ntiles = (uint32_t)(1ull << (n - T));
-    for (int m = 0; m < K; ++m) a.cfg_basis[m] = swz(8u << tpos[m]);
-    a.pair = tpos[0] == 0;
-    // lane bits: the ordering of the 7 row qubits with the fewest modelled wavefronts
-    {
-        int perm[7] = {0, 1, 2, 3, 4, 5, 6}, best[7];
-        int bestw = 1 << 30;
+    a.pair = (mmask & 1ull) != 0;  // qubit 0 (tile bit 0) is matrix bit 0
+    // Tile layout in shared memory = the TMA box's dimension order: qubits 0..3 (128-byte
+    // rows), then the middle dimensions (runs of consecutive qubits, <= 8 qubits each, at
+    // most three), then the boxes of the remaining high matrix qubits.  "natural" keeps the
+    // low run in qubit order; "rows first" puts the runs of row qubits right after qubits
+    // 0..3 so that they land on the swizzled bank bits (matrix qubits 4, 5, ... otherwise
+    // push the row qubits above them and every lane of a quarter-warp hits the same bank
+    // group).  The layout with fewer modelled wavefronts wins.
+    struct Layout {
+        std::vector<std::pair<int, int>> segs;  // middle dims (first qubit, length)
+        std::vector<int> ops;                   // high matrix qubits enumerated by boxes
+        int pos[64];
+        int perm[7];
+        int wf = 1 << 30;
+        bool ok = false;
+    };
+    auto build = [&](bool rows_first, Layout& Lo) {
+        std::vector<std::pair<int, int>> low;  // runs of qubits 4..L-1 (row runs first if asked)
+        for (int pass = 0; pass < (rows_first ? 2 : 1); ++pass)
+            for (int q = 4; q < L;) {
+                const bool isrow = !((mmask >> q) & 1);
+                int e = q + 1;
+                while (e < L && (rows_first ? (!((mmask >> e) & 1)) == isrow : true)) ++e;
+                if (!rows_first || isrow == (pass == 0)) low.push_back({q, e - q});
+                q = e;
+            }
+        for (auto& r : low)
+            for (int q = r.first; q < r.first + r.second; q += 8) Lo.segs.push_back({q, std::min(8, r.first + r.second - q)});
+        if (Lo.segs.size() > 3) return;
+        size_t hi = 0;
+        while (Lo.segs.size() < 3 && hi < high.size()) Lo.segs.push_back({high[hi++], 1});
+        for (; hi < high.size(); ++hi) Lo.ops.push_back(high[hi]);
+        int p = 0;
+        for (int q = 0; q < 4; ++q) Lo.pos[q] = p++;
+        for (auto& sg : Lo.segs)
+            for (int q = sg.first; q < sg.first + sg.second; ++q) Lo.pos[q] = p++;
+        for (int q : Lo.ops) Lo.pos[q] = p++;
+        // lane bits: the ordering of the 7 row qubits with the fewest modelled wavefronts
+        int perm[7] = {0, 1, 2, 3, 4, 5, 6};
         do {
             uint32_t off[32];
             for (int l = 0; l < 32; ++l) {
                 uint32_t o = 0;
                 for (int j = 0; j < 5; ++j)
-                    if ((l >> j) & 1) o ^= swz(8u << rowq[perm[j]]);
+                    if ((l >> j) & 1) o ^= swz(8u << Lo.pos[rowq[perm[j]]]);
                 off[l] = o;
             }
             const int w = wavefronts(off, a.pair ? 16 : 8);
-            if (w < bestw) {
-                bestw = w;
-                std::copy(perm, perm + 7, best);
+            if (w < Lo.wf) {
+                Lo.wf = w;
+                std::copy(perm, perm + 7, Lo.perm);
             }
         } while (std::next_permutation(perm, perm + 7));
-        for (int j = 0; j < 7; ++j) a.row_basis[j] = swz(8u << rowq[best[j]]);
-    }
-    // tensor map: [0..3] [4..L-1] (split at 8 bits) [high dims] ... [rest]
+        Lo.ok = true;
+    };
+    Layout nat, rf;
+    build(false, nat);
+    build(true, rf);
+    const Layout& Lo = (rf.ok && (!nat.ok || rf.wf < nat.wf)) ? rf : nat;
+    if (!Lo.ok) return false;
+    for (int m = 0; m < K; ++m) a.cfg_basis[m] = swz(8u << Lo.pos[mq[m]]);
+    for (int j = 0; j < 7; ++j) a.row_basis[j] = swz(8u << Lo.pos[rowq[Lo.perm[j]]]);
+    // tensor map: [0..3] [middle dims] (size-1 fillers) [rest]
     cuuint64_t dims[5], strides[4];
     cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
     int nd = 0;
     dims[nd] = 16;
     box[nd++] = 16;
-    const int rem = L - 4;
-    if (rem <= 8) {
-        dims[nd] = 1ull << rem;
-        strides[nd - 1] = 128;
-        box[nd++] = 1u << rem;
-    } else {
-        dims[nd] = 256;
-        strides[nd - 1] = 128;
-        box[nd++] = 256;
-        dims[nd] = 1ull << (rem - 8);
-        strides[nd - 1] = 128ull << 8;
-        box[nd++] = 1u << (rem - 8);
-    }
-    const int hd = std::min((int)high.size(), 4 - nd);
-    for (int i = 0; i < hd; ++i) {
-        dims[nd] = 2;
-        strides[nd - 1] = 8ull << high[i];
-        box[nd++] = 2;
+    for (auto& sg : Lo.segs) {
+        dims[nd] = 1ull << sg.second;
+        strides[nd - 1] = 8ull << sg.first;
+        box[nd++] = 1u << sg.second;
     }
     while (nd < 4) {
         dims[nd] = 1;
@@ -544,13 +567,13 @@ static bool plan_gate(void* state, int n, int nq, const int* qs, const cd* U, Gs
     dims[4] = 1ull << (n - L);
     strides[3] = 8ull << L;
     box[4] = 1;
-    const int extra = (int)high.size() - hd;
+    const int extra = (int)Lo.ops.size();
     a.nops = 1 << extra;
     a.op_bytes = (uint32_t)((128u << K) * 8u) >> extra;
     for (int o = 0; o < a.nops; ++o) {
         int32_t r = 0;
         for (int i = 0; i < extra; ++i)
-            if ((o >> i) & 1) r += (int32_t)(1u << (high[hd + i] - L));
+            if ((o >> i) & 1) r += (int32_t)(1u << (Lo.ops[i] - L));
         a.op_rest[o] = r;
     }
     EncodeTiledFn enc = encode_fn();
