@@ -261,11 +261,30 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// Block-sum heap of a slot (registers with many tiles): node 1 = the whole state, node i's
+// children 2i, 2i + 1 = its lower / upper half, leaves 2^(n-T) + tile = the block sums, so
+// the sampler's global levels read two nodes per level instead of re-summing the leaves of
+// the current prefix for every shot (pairwise sums, fp64).
+__global__ void __launch_bounds__(256) blocksum_heap_kernel(const double* __restrict__ blocksum, int lg,
+                                                            double* __restrict__ heap) {
+    const uint64_t nt = 1ull << lg;
+    const double* bs = blocksum + (uint64_t)blockIdx.x * nt;
+    double* h = heap + (uint64_t)blockIdx.x * 2 * nt;
+    for (uint64_t i = threadIdx.x; i < nt; i += blockDim.x) h[nt + i] = bs[i];
+    __syncthreads();
+    for (int d = lg - 1; d >= 0; --d) {
+        const uint64_t b = 1ull << d;
+        for (uint64_t i = b + threadIdx.x; i < 2 * b; i += blockDim.x) h[i] = h[2 * i] + h[2 * i + 1];
+        __syncthreads();
+    }
+}
+
 __global__ void __launch_bounds__(128)
 sample_kernel(const float2* __restrict__ state, int n, int T, const double* __restrict__ blocksum,
               int nslots, int shots, uint64_t seed, const uint64_t* __restrict__ traj_ids,
               const double* __restrict__ p00, const double* __restrict__ p11,
-              uint64_t* __restrict__ out_bits, int n_rng, const int32_t* __restrict__ shot_ids) {
+              uint64_t* __restrict__ out_bits, int n_rng, const int32_t* __restrict__ shot_ids,
+              const double* __restrict__ heap) {
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (gw >= nslots * shots) return;
@@ -282,12 +301,20 @@ sample_kernel(const float2* __restrict__ state, int n, int T, const double* __re
     for (int l = n - 1; l >= T; --l) {
         const uint64_t half = 1ull << (l - T);
         double m0 = 0.0, m1 = 0.0;
-        for (uint64_t i = lane; i < half; i += 32) {
-            m0 += bs[lo + i];
-            m1 += bs[lo + half + i];
+        if (heap) {
+            // node of the current prefix at depth n - 1 - l, its two children
+            const double* h = heap + (uint64_t)slot * 2 * ntiles;
+            const uint64_t node = (1ull << (n - 1 - l)) + (lo >> (l - T + 1));
+            m0 = h[2 * node];
+            m1 = h[2 * node + 1];
+        } else {
+            for (uint64_t i = lane; i < half; i += 32) {
+                m0 += bs[lo + i];
+                m1 += bs[lo + half + i];
+            }
+            m0 = warp_sum(m0);
+            m1 = warp_sum(m1);
         }
-        m0 = warp_sum(m0);
-        m1 = warp_sum(m1);
         const double u = draw(seed, (uint32_t)(shot * half_n + l / 2), kPurposeSample, traj, l & 1);
         int bit;
         if (m0 == 0.0) bit = 1;
@@ -338,13 +365,14 @@ sample_kernel(const float2* __restrict__ state, int n, int T, const double* __re
 cudaError_t launch_sample(const float2* state, int n, int T, const double* blocksum, int nslots,
                           int shots, uint64_t seed, const uint64_t* traj_ids, const double* p00,
                           const double* p11, uint64_t* out_bits, cudaStream_t s, int n_rng,
-                          const int32_t* shot_ids) {
+                          const int32_t* shot_ids, double* heap) {
     const long warps = (long)nslots * shots;
     if (warps <= 0) return cudaSuccess;
+    if (heap) blocksum_heap_kernel<<<nslots, 256, 0, s>>>(blocksum, n - T, heap);
     const int threads = 128;
     const long blocks = (warps * 32 + threads - 1) / threads;
     sample_kernel<<<(unsigned)blocks, threads, 0, s>>>(state, n, T, blocksum, nslots, shots, seed,
-                                                       traj_ids, p00, p11, out_bits, n_rng, shot_ids);
+                                                       traj_ids, p00, p11, out_bits, n_rng, shot_ids, heap);
     return cudaGetLastError();
 }
 

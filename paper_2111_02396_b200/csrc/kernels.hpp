@@ -59,7 +59,9 @@ cudaError_t launch_init_states(float2* state, int n, int nslots, cudaStream_t s)
 cudaError_t launch_sample(const float2* state, int n, int T, const double* blocksum, int nslots,
                           int shots, uint64_t seed, const uint64_t* traj_ids, const double* p00,
                           const double* p11, uint64_t* out_bits, cudaStream_t s, int n_rng = 0,
-                          const int32_t* shot_ids = nullptr);
+                          const int32_t* shot_ids = nullptr, double* heap = nullptr);
+// registers with at least 2^kHeapMinLg tiles sample through a block-sum heap (2 x tiles doubles per slot)
+constexpr int kHeapMinLg = 10;
 
 // dst[pi(i)] = src[i] where bit b of i moves to bit perm[b] (n <= 24).
 cudaError_t launch_permute_qubits(const float2* src, float2* dst, int n, const int* perm, cudaStream_t s);

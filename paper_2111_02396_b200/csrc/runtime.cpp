@@ -90,7 +90,7 @@ struct HostBuf {
 // Per-batch device + staging buffers (two of them for pipelining).
 struct BatchBufs {
     DevBuf pass_start, pass_count, passes, gates, fused, cons, events, pool, records, traj_ids,
-        bits, obs_out, status, counters, rho_part, blocksum, obs_part, slot_list;
+        bits, obs_out, status, counters, rho_part, blocksum, obs_part, slot_list, heap;
     HostBuf h_blob, h_out;
     cudaEvent_t done = nullptr;
     cudaEvent_t prepared = nullptr;  // uploads + materialization of this batch (prep stream)
@@ -102,7 +102,7 @@ struct BatchBufs {
     void release() {
         for (DevBuf* b : {&pass_start, &pass_count, &passes, &gates, &fused, &cons, &events, &pool,
                           &records, &traj_ids, &bits, &obs_out, &status, &counters, &rho_part,
-                          &blocksum, &obs_part, &slot_list})
+                          &blocksum, &obs_part, &slot_list, &heap})
             b->release();
         h_blob.release();
         h_out.release();
@@ -462,9 +462,14 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
         ++launches;
     }
     if (want_bits && shots > 0) {
+        double* heap = nullptr;
+        if (n - T >= kHeapMinLg) {
+            QT_CK(B.heap.ensure(sizeof(double) * 2 * (size_t)nslots * ntiles));
+            heap = B.heap.as<double>();
+        }
         QT_CK(launch_sample(state, n, T, B.blocksum.as<double>(), nslots, shots, seed, B.traj_ids.as<uint64_t>(),
                             P.has_p00 ? ctx->p00.as<double>() : nullptr, P.has_p11 ? ctx->p11.as<double>() : nullptr,
-                            B.bits.as<uint64_t>(), s));
+                            B.bits.as<uint64_t>(), s, 0, nullptr, heap));
         ++launches;
     }
     if (st) st->launches += launches;
@@ -801,8 +806,13 @@ static qt_status run_single(qt_ctx ctx, qt_plan plan, float2* state, const ObsGr
             QT_CK(cudaMemcpyAsync(B.counters.p, ex->shot_ids, sizeof(int32_t) * shots, cudaMemcpyHostToDevice, s));
             dshots = B.counters.as<int32_t>();
         }
+        double* heap = nullptr;
+        if (n - T >= kHeapMinLg) {
+            QT_CK(B.heap.ensure(sizeof(double) * 2 * (size_t)ntiles));
+            heap = B.heap.as<double>();
+        }
         QT_CK(launch_sample(state, n, T, B.blocksum.as<double>(), 1, shots, seed, B.traj_ids.as<uint64_t>(), nullptr,
-                            nullptr, B.bits.as<uint64_t>(), s, ex ? ex->n_rng : 0, dshots));
+                            nullptr, B.bits.as<uint64_t>(), s, ex ? ex->n_rng : 0, dshots, heap));
     }
     std::vector<double> obs_host(std::max(n_obs, 1));
     if (out_obs && n_obs > 0)

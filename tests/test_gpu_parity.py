@@ -212,6 +212,21 @@ def test_sample_and_expectation_standalone(ctx):
             assert abs(ev[k] - oracle.pauli_expectation(psi, s)) < OBS_TOL
 
 
+def test_sample_block_sum_heap(ctx):
+    """Registers of >= 2^10 tiles sample their global levels through the block-sum heap
+    (kernels.cu blocksum_heap_kernel): bitstrings identical to the oracle's chain rule,
+    standalone (n = 24) and at the end of trajectories (n = 23, 4 shots each)."""
+    rng = np.random.default_rng(8)
+    n = 24
+    psi = rand_state(rng, n)
+    got = ctx.sample_bitstrings(to_dev(psi), seed=4, traj=7, shots=256)
+    ref, mg = oracle.sample_state(psi.astype(np.complex64).astype(np.complex128), seed=4, traj=7, shots=256)
+    assert not [i for i in np.flatnonzero(got != ref) if mg[i] >= MARGIN]
+    c = workloads.random_circuit(23, depth=3, seed=31, max_arity=2, noise="depol", p=0.02)
+    ref, out, state = run_both(ctx, c, seed=3, T=2, shots=4, f=4)
+    compare(ref, out, state)
+
+
 def test_config2_sample_of_trajectories(ctx):
     """C2 (20 q Sycamore-style + QCS-like noise) on 4 trajectory indices spread
     over [0, 1e4): the launch configuration bench.py times (f=4, tiles)."""
