@@ -810,9 +810,12 @@ tile_pass_kernel(const TileArgs A, const int step) {
         } else {
             rho_partial<1, T, NT>(tile, ql, out, red);
         }
-        __threadfence();
+        // writers ordered before thread 0 by the barrier; its device-scope fence releases them
         __syncthreads();
-        if (tid == 0) s_last = (atomicAdd(&A.counters[slot], 1) == (int)ntiles - 1);
+        if (tid == 0) {
+            __threadfence();
+            s_last = (atomicAdd(&A.counters[slot], 1) == (int)ntiles - 1);
+        }
         __syncthreads();
         if (s_last) {
             // last CTA of the slot: sum the tile partials with every thread (tiles

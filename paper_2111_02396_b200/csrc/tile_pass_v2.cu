@@ -845,9 +845,14 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                 if (P.rho_nq == 1) rho_partial<1>(tile, ql, out, red, wg);
                 else if (P.rho_nq == 2) rho_partial<2>(tile, ql, out, red, wg);
                 else rho_partial_rows3(tile, ql, out, red, wg);
-                __threadfence();
+                // the partial's writers are ordered before thread 0 by the barrier, and thread
+                // 0's device-scope fence before the counter increment releases them
+                // cumulatively (one fence per warpgroup instead of one per thread)
                 bar_wg(wg);
-                if (wtid == 0) misc[1 + wg] = (atomicAdd(&A.counters[slot], 1) == (int)ntiles - 1);
+                if (wtid == 0) {
+                    __threadfence();
+                    misc[1 + wg] = (atomicAdd(&A.counters[slot], 1) == (int)ntiles - 1);
+                }
                 bar_wg(wg);
                 if (misc[1 + wg]) {
                     // last tile of the slot: sum the tile partials in a fixed order, then choose
