@@ -135,6 +135,12 @@ qt_status fail(qt_status st, const std::string& m) {
     return st;
 }
 
+// registers of >= 2^heap_min_lg() tiles sample through the block-sum heap (QT_HEAP_MIN_LG overrides)
+int heap_min_lg() {
+    static const int v = getenv("QT_HEAP_MIN_LG") ? atoi(getenv("QT_HEAP_MIN_LG")) : kHeapMinLg;
+    return v;
+}
+
 template <class F>
 void parallel_for(int count, int threads, F&& fn) {
     threads = std::max(1, std::min(threads, count));
@@ -460,10 +466,21 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
         QT_CK(launch_finalize_obs(B.blocksum.as<double>(), B.obs_part.as<double>(), (int)ntiles, n_obs, nslots,
                                   B.obs_out.as<double>(), nullptr, s));
         ++launches;
+        if (const char* dump = std::getenv("QT_DUMP_PARTIALS")) {  // diagnostics: block sums + observable partials
+            std::vector<double> hb((size_t)nslots * ntiles), ho((size_t)nslots * ntiles * n_obs);
+            cudaMemcpyAsync(hb.data(), B.blocksum.p, hb.size() * 8, cudaMemcpyDeviceToHost, s);
+            cudaMemcpyAsync(ho.data(), B.obs_part.p, ho.size() * 8, cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            if (FILE* f = std::fopen(dump, "wb")) {
+                std::fwrite(hb.data(), 8, hb.size(), f);
+                std::fwrite(ho.data(), 8, ho.size(), f);
+                std::fclose(f);
+            }
+        }
     }
     if (want_bits && shots > 0) {
         double* heap = nullptr;
-        if (n - T >= kHeapMinLg) {
+        if (n - T >= heap_min_lg()) {
             QT_CK(B.heap.ensure(sizeof(double) * 2 * (size_t)nslots * ntiles));
             heap = B.heap.as<double>();
         }
@@ -807,7 +824,7 @@ static qt_status run_single(qt_ctx ctx, qt_plan plan, float2* state, const ObsGr
             dshots = B.counters.as<int32_t>();
         }
         double* heap = nullptr;
-        if (n - T >= kHeapMinLg) {
+        if (n - T >= heap_min_lg()) {
             QT_CK(B.heap.ensure(sizeof(double) * 2 * (size_t)ntiles));
             heap = B.heap.as<double>();
         }

@@ -416,14 +416,27 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
     unsigned char* sm = smem_raw + (((raw_s + 1023u) & ~1023u) - raw_s);
     const uint32_t sm_s = (uint32_t)__cvta_generic_to_shared(sm);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t mb = sm_s + kMbarOff;  // full[3], empty[3], mma[2], wfull[2][2]
-    auto full_bar = [&](int b) { return mb + 8u * (uint32_t)b; };
+    const uint32_t mb = sm_s + kMbarOff;  // full[3] (use 0), empty[3], mma[2], wfull[2][2], full[3] (use 1)
+    // "full" barriers: item jj (buffer jj % 3, warpgroup jj % 2) completes on barrier
+    // [jj % 3][(jj / 3) & 1], phase (jj / 6) & 1.  A buffer's successive occupants belong
+    // to alternating warpgroups, so with one barrier per buffer a warpgroup could wait for
+    // the phase after next while the other warpgroup's load (the phase in between) is
+    // still in flight, see the parity of an old phase and read the buffer early (it did:
+    // read-only passes of n = 23 registers gave wrong observables).  With two barriers per
+    // buffer each one is waited on by a single warpgroup, in phase order.
+    auto full_bar = [&](int jj) {
+        const int b = jj % NBUF, u = (jj / NBUF) & 1;
+        return mb + 8u * (uint32_t)(u ? 12 + b : b);
+    };
     auto mma_bar = [&](int w) { return mb + 8u * (uint32_t)(6 + w); };
     auto wfull_bar = [&](int w, int i) { return mb + 8u * (uint32_t)(8 + 2 * w + i); };
     uint32_t* misc = reinterpret_cast<uint32_t*>(sm + kMiscOff);  // [0] tmem base, [1..2] last flags
     if (warp == 0) tc::tmem_alloc(misc, 512);
     if (tid == 32) {
-        for (int b = 0; b < NBUF; ++b) mbar_init_s(full_bar(b), NT);
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init_s(full_bar(b), NT);
+            mbar_init_s(full_bar(b + NBUF), NT);
+        }
         for (int w = 0; w < NWG; ++w) {
             mbar_init_s(mma_bar(w), 4);  // one commit per issuing warp
             mbar_init_s(wfull_bar(w, 0), QT_V2_BULKW ? 1 : NT);
@@ -449,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
             float4* t4 = reinterpret_cast<float4*>(sm + (size_t)b * kTileBytes);
             for (int k = wtid; k < TILE / 2; k += NT)
                 t4[k] = make_float4((k == 0 && tile == 0) ? 1.f : 0.f, 0.f, 0.f, 0.f);
-            mbar_arrive_s(full_bar(b));
+            mbar_arrive_s(full_bar(jj));
         } else {
             const float2* st = A.state + ((uint64_t)P.slot << n) + tbase_g;
             // thread: pair p = wtid & 7 of run h = 32 k + (wtid >> 3); h bits 0..4 fixed
@@ -469,7 +482,13 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                 const uint64_t x = ((k & 2) ? e1 : 0ull) + ((k & 4) ? e2 : 0ull) + ((k & 8) ? e3 : 0ull);
                 cp_async16_s(buf + 8u * slot, ((k & 1) ? s1 : src) + x);
             }
-            cp_async_arrive_noinc(full_bar(b));
+            // the loading threads wait for their own copies, then arrive: completion by
+            // cp.async.mbarrier.arrive.noinc let consumers pass the phase with part of the
+            // tile not yet written (read-only passes of n = 23 registers, about one tile in
+            // 4000, measured with QT_DUMP_PARTIALS); waiting here cost nothing measurable
+            // on C2 (110.4 vs 110.9 ms per 1024 trajectories)
+            asm volatile("cp.async.wait_all;\n" ::: "memory");
+            mbar_arrive_s(full_bar(jj));
         }
     };
     {
@@ -615,7 +634,7 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
             // every thread acquires the tile's "full" phase (the cp.async writes of the
             // loading warpgroup; a single poller + bar.sync would order them too, but
             // compute-sanitizer racecheck only tracks the direct acquire)
-            mbar_wait_s(full_bar(b), (uint32_t)((jj / NBUF) & 1));
+            mbar_wait_s(full_bar(jj), (uint32_t)((jj / (2 * NBUF)) & 1));
             QT_T(0);
             QT_C(11, 1);
             float run_inv = 1.f;
