@@ -48,6 +48,7 @@ struct GsArgs {
     uint32_t cfg_basis[6];  // swizzled tile byte offset of matrix bit m
     int32_t op_rest[16];    // rest coordinate (units of 2^L amplitudes) of box o
     int pair;               // matrix bit 0 is tile bit 0: configurations 2i, 2i + 1 form one 16-byte pair
+    int reps;               // applications per tile (1; > 1 only in the QT_GS_REPS experiment)
 };
 
 template <int K>
@@ -283,6 +284,10 @@ __global__ void __launch_bounds__(Cfg<K>::THREADS, 1) __maxnreg__(Cfg<K>::MAXREG
             __syncwarp();
             GS_PROG(2);  // the tcgen05 .sync.aligned operations below need converged warps
             unsigned char* tile = sm + (size_t)s * C::TILE_BYTES;
+            // (experiment: a.reps > 1 applies the gate reps times per tile -- the cost of
+            // several gates per HBM pass in this pipeline; tools/gs_reps.py)
+            for (int rep = 0; rep < a.reps; ++rep) {
+            if (rep) bar_wg(wg);  // the previous application's write-backs are visible
             // ---- gather the row's 2^K amplitudes, per-row power-of-two scale ----
             auto load16 = [&](int c0, float2 (&v)[16]) {
                 if (pair) {
@@ -378,6 +383,7 @@ __global__ void __launch_bounds__(Cfg<K>::THREADS, 1) __maxnreg__(Cfg<K>::MAXREG
                             make_float2(__uint_as_float(d[2 * c]) * inv, __uint_as_float(d[2 * c + 1]) * inv);
                 }
             }
+            }  // rep
             tc::fence_before();
             tc::fence_proxy_async();  // generic writes -> the TMA store (async proxy)
             arrive(bar + 8u * (C::STAGES + s));
@@ -487,6 +493,7 @@ static bool plan_gate(void* state, int n, int nq, const int* qs, const cd* U, Gs
     for (int h : high) a.tile_mask |= 1ull << h;
     a.ntiles = (uint32_t)(1ull << (n - T));
     a.pair = (mmask & 1ull) != 0;  // qubit 0 (tile bit 0) is matrix bit 0
+    a.reps = getenv("QT_GS_REPS") ? std::max(1, atoi(getenv("QT_GS_REPS"))) : 1;
     // Tile layout in shared memory = the TMA box's dimension order: qubits 0..3 (128-byte
     // rows), then the middle dimensions (runs of consecutive qubits, <= 8 qubits each, at
     // most three), then the boxes of the remaining high matrix qubits.  "natural" keeps the
