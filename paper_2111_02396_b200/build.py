@@ -9,7 +9,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.environ.get("QT_LIB_OUT", os.path.join(HERE, "libqtraj.so"))
 OBJ = os.path.join(HERE, "build_obj" + os.environ.get("QT_OBJ_SUFFIX", ""))
 SOURCES = ["tile_pass_r4.cu", "tile_pass_r5.cu", "tile_pass_r6.cu", "tile_pass_tc.cu", "tile_pass_tcw.cu",
-           "tile_pass_v2.cu", "gate_stream.cu", "tile_pass_r5s.cu", "tile_pass_r6s_a.cu", "tile_pass_r6s_b.cu", "kernels.cu",
+           "tile_pass_v2.cu", "tile_pass_v3.cu", "gate_stream.cu", "tile_pass_r5s.cu", "tile_pass_r6s_a.cu", "tile_pass_r6s_b.cu", "kernels.cu",
            "circuit.cpp", "planner.cpp", "runtime.cpp", "dist_host.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

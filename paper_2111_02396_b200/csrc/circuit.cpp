@@ -166,7 +166,8 @@ void cuda_core_plan(Plan& P) {
     for (const PlanOp& op : P.ops) max_arity = std::max(max_arity, op.nq);
     P.tc = false;
     P.v2 = false;
-    if (P.T == 13) P.T = 12;
+    if (P.T == 13 || (P.v3 && P.n >= 12)) P.T = 12;
+    P.v3 = false;
     if (P.T >= 12) {
         P.R = std::max(P.f <= 4 ? 4 : P.f, max_arity);
     } else {
@@ -461,6 +462,15 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
     // (QT_TILE13=0 selects the per-tile kernel instead, for A/B measurements)
     const char* env13 = std::getenv("QT_TILE13");
     const bool auto13 = !(env13 && env13[0] == '0');
+    // tile_bits = 11: the TMA-pipelined kernel (tile_pass_v3.cu) on 11-qubit tiles
+    const bool v3_ok = C.n >= 12 && o.tensor_cores >= 0 && f <= 4 && max_arity <= f && o.low_bits == 0;
+    if (o.tile_bits == 11 && C.n >= 12) {
+        if (!v3_ok) {
+            delete hp;
+            return fail(QT_EINVAL, "tile_bits = 11 needs n >= 12, tensor cores and max_fused <= 4");
+        }
+        P.v3 = true;
+    }
     P.T = o.tile_bits ? o.tile_bits : std::min(C.n, (v2_ok && auto13) ? 13 : 12);
     if (P.T == 13 && !v2_ok) {
         delete hp;
@@ -470,7 +480,7 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
         delete hp;
         return fail(QT_EINVAL, "tile_bits must be <= min(n, 12), or 13");
     }
-    if (C.n > 12 && P.T != 12 && P.T != 13) {
+    if (C.n > 12 && P.T != 12 && P.T != 13 && !P.v3) {
         delete hp;
         return fail(QT_EINVAL, "tile_bits must be 12 or 13 for n > 12 in this build");
     }
@@ -485,7 +495,7 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
     P.one_gate = o.one_gate_per_pass != 0;
     // tensor cores: every fused gate padded to 4 qubits (f <= 4), T = 12, 128-thread CTAs
     // whose CUDA-core gates use R = 5
-    const bool tc_ok = ((P.T == 12 || P.T == 13) && max_arity <= f);
+    const bool tc_ok = ((P.T == 12 || P.T == 13 || P.v3) && max_arity <= f);
     if (o.tensor_cores > 0 && !tc_ok) {
         delete hp;
         return fail(QT_EINVAL, "tensor_cores needs n >= 12 and gates of <= max_fused qubits");
@@ -505,6 +515,8 @@ qt_status qt_fuse_ex(qt_circuit c, const qt_fuse_opts* opts, qt_plan* out) {
             P.v2 = true;
             P.R = 5;
         }
+        // T = 11: 128 threads per warpgroup hold 16 amplitudes each (a row of a gate)
+        if (P.v3) P.R = 4;
     }
     // canonical order: moment ascending, then call order (stable)
     std::vector<const HostOp*> order;

@@ -75,6 +75,7 @@ struct Plan {
     bool one_gate = false;
     bool tc = false;    // fused gates padded to tc_k qubits and applied on tcgen05 tensor cores
     int tc_k = 4;       // 4 (f <= 4), 5 (f = 5) or 6 (f = 6)
+    bool v3 = false;    // tile_bits = 11: TMA-pipelined kernel (tile_pass_v3.cu), 4-qubit tensor-core gates
     bool v2 = false;    // tc_k == 4 on n >= 13 qubits: T = 13 tiles, persistent TMEM kernel (tile_pass_v2.cu)
     std::vector<PlanOp> ops;
     std::vector<Variant> vars;

@@ -48,6 +48,7 @@ cudaError_t launch_tile_pass(const TileArgs& a, int R, int tck, int step, uint32
     // T = 1..11 (the whole state of n < 12 qubits in one CTA) and (T, 5 | 6) for
     // T = R..11 (5- and 6-qubit gates on small registers); tensor cores
     // (tck = 4, 5 or 6 qubits per padded gate): (12, 5).
+    if (a.T == 11 && a.v3maps) return tck == 4 ? launch_tile_pass_v3(a, a.v3maps, step, ntiles, nslots, s) : cudaErrorInvalidValue;
     if (a.T == 13) return tck == 4 ? launch_tile_pass_v2(a, step, ntiles, nslots, s) : cudaErrorInvalidValue;
     if (tck) return a.T == 12 && R == 5 ? launch_tile_pass_tc(a, tck, step, ntiles, nslots, s) : cudaErrorInvalidValue;
     if (a.T == 12 && R == 6) return launch_tile_pass_r6(a, step, ntiles, nslots, s);

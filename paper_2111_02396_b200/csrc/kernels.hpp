@@ -1,5 +1,6 @@
 // kernels.hpp -- launch interface of the sm_100a kernels (kernels.cu).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -34,7 +35,21 @@ struct TileArgs {
     const ObsDesc* obs;
     uint32_t prefetch;          // L2-prefetch the tile this many CTAs ahead (0 = off; set by the launcher)
     unsigned long long* timing = nullptr;  // -DQT_TIMING builds: clock64 phase sums (diagnostics)
+    const void* v3maps = nullptr;          // T = 11 (tile_pass_v3.cu): V3Map per tile layout (PassDesc::pad)
 };
+
+// TMA description of one 11-qubit tile layout over a batch buffer (tile_pass_v3.cu):
+// 5-D tensor map [qubits 0..3 | up to three runs of tile qubits | rest (16 amplitudes)],
+// plus the boxes enumerating the tile qubits outside those runs.
+struct alignas(64) V3Map {
+    CUtensorMap tm;
+    int32_t nops;
+    uint32_t op_bytes;
+    int32_t op_rest[16];  // rest-coordinate offset of box o
+};
+bool v3_encode_map(void* state, int n, uint64_t nslots, uint64_t tile_mask, V3Map* out);
+cudaError_t launch_tile_pass_v3(const TileArgs& a, const void* maps, int step, uint32_t ntiles, int nslots,
+                                cudaStream_t s);
 
 // Largest register width R (amplitudes per thread = 2^R) compiled.
 constexpr int kMaxR = 6;

@@ -613,6 +613,44 @@ inline unsigned v2_bank(int b) {  // slot bits 0..3 of tile bit b under the T = 
 }
 }  // namespace
 
+// TMA-pipelined kernel (tile_pass_v3.cu, T = 11): the 7 thread bits (tpos) of a gate,
+// reordered so that a warp's lanes reach distinct shared-memory banks under the TMA
+// SWIZZLE_128B image (tile bit b -> 8-byte bank-pair bit b for b < 4, bits 4..6 fold onto
+// pair bits 1..3, bits >= 7 none): 16-byte pair accesses (matrix bit 0 = tile bit 0) are
+// served per quarter warp (lanes 0..2 must cover pair bits 1, 2, 3), 8-byte accesses per
+// half warp (lanes 0..3: pair bits 0..3).
+void v3_lanes(GateDesc& gd) {
+    int rows[7], nr = 0;
+    for (int i = 0; i < 7; ++i) rows[nr++] = (int)((gd.tpos >> (4 * i)) & 15u);
+    const bool pair = (gd.k & kGateTC) && (gd.rpos & 15u) == 0u;
+    bool used[7] = {false, false, false, false, false, false, false};
+    int order[7], no = 0;
+    auto take = [&](int b) {
+        for (int i = 0; i < 7; ++i)
+            if (!used[i] && rows[i] == b) {
+                used[i] = true;
+                order[no++] = b;
+                return true;
+            }
+        return false;
+    };
+    if (!pair) take(0);
+    for (int c = 1; c <= 3; ++c)
+        if (!take(c)) take(c + 3);
+    for (int i = 0; i < 7; ++i)
+        if (!used[i]) {
+            used[i] = true;
+            order[no++] = rows[i];
+        }
+    gd.tpos = 0;
+    for (int i = 0; i < 7; ++i) gd.tpos |= (uint32_t)order[i] << (4 * i);
+    // swizzled byte offsets of the roles for the kernel: xu[0..3] register / matrix bits
+    // (rpos), xu[4..10] thread bits (tpos)
+    auto swzb = [](int b) { const uint32_t x = 8u << b; return (uint16_t)(x ^ (((x >> 7) & 7u) << 4)); };
+    for (int m = 0; m < 4; ++m) gd.xu[m] = swzb((int)((gd.rpos >> (4 * m)) & 15u));
+    for (int i = 0; i < 7; ++i) gd.xu[4 + i] = swzb(order[i]);
+}
+
 // Layout roles of a v2 gate: the tile bits of its matrix bits (cfg, in matrix-bit
 // order), of its two group bits, of the 5 TMEM lane bits and of the 2 warp bits.
 struct V2Lay {
@@ -1052,10 +1090,10 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
                     const uint64_t pm = padded(g);
                     const int d = 1 << popc(pm);
                     // tensor cores: the GEMM operand, tc_gate_bytes(tc_k) bytes (complex64 units)
-                    gd.mat_off = alloc(P.v2 ? kV2GateBytes / 8 : (P.tc ? tc_gate_bytes(P.tc_k) / 8 : d * d));
+                    gd.mat_off = alloc((P.v2 || P.v3) ? kV2GateBytes / 8 : (P.tc ? tc_gate_bytes(P.tc_k) / 8 : d * d));
                     FusedDesc fd;
                     fd.mat_off = gd.mat_off;
-                    fd.k = popc(pm) | (P.tc ? kGateTC : 0) | (P.v2 ? kGateV2 : 0);
+                    fd.k = popc(pm) | (P.tc ? kGateTC : 0) | ((P.v2 || P.v3) ? kGateV2 : 0);
                     fd.cons_begin = (int32_t)out.cons.size();
                     fd.cons_count = (int32_t)g.n_items;
                     for (int it : g) {
@@ -1138,6 +1176,8 @@ qt_status plan_trajectory(const Plan& P, uint64_t seed, uint64_t traj, const Obs
                 }
                 v2_layouts(out.gates.data() + pd.gate_begin, lm.data(), gate_norms.data() + pd.gate_begin,
                            pd.gate_count, out.fused, out.cons, gate_fused.data() + pd.gate_begin);
+            } else if (P.v3) {
+                for (int g = 0; g < pd.gate_count; ++g) v3_lanes(out.gates[pd.gate_begin + g]);
             } else if (P.tc && P.tc_k == 4) {
                 tc_runs(out.gates.data() + pd.gate_begin, gate_norms.data() + pd.gate_begin, pd.gate_count, T,
                         out.fused, out.cons, gate_fused.data() + pd.gate_begin);

@@ -90,7 +90,7 @@ struct HostBuf {
 // Per-batch device + staging buffers (two of them for pipelining).
 struct BatchBufs {
     DevBuf pass_start, pass_count, passes, gates, fused, cons, events, pool, records, traj_ids,
-        bits, obs_out, status, counters, rho_part, blocksum, obs_part, slot_list, heap;
+        bits, obs_out, status, counters, rho_part, blocksum, obs_part, slot_list, heap, maps;
     HostBuf h_blob, h_out;
     cudaEvent_t done = nullptr;
     cudaEvent_t prepared = nullptr;  // uploads + materialization of this batch (prep stream)
@@ -102,7 +102,7 @@ struct BatchBufs {
     void release() {
         for (DevBuf* b : {&pass_start, &pass_count, &passes, &gates, &fused, &cons, &events, &pool,
                           &records, &traj_ids, &bits, &obs_out, &status, &counters, &rho_part,
-                          &blocksum, &obs_part, &slot_list, &heap})
+                          &blocksum, &obs_part, &slot_list, &heap, &maps})
             b->release();
         h_blob.release();
         h_out.release();
@@ -365,6 +365,29 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
                 h_sl[k] = h_pass[h_ps[b] + step];
                 h_sl[k++].slot = b;
             }
+    // T = 11 (tile_pass_v3.cu): one tensor map per distinct tile layout of the batch
+    // (over the batch buffer), its index in PassDesc::pad of the launch arrays
+    std::vector<V3Map> v3m;
+    if (P.v3) {
+        std::vector<std::pair<uint64_t, int>> seen;
+        for (int k = 0; k < step_off[maxp]; ++k) {
+            const uint64_t m = h_sl[k].tile_mask;
+            int id = -1;
+            for (auto& sp : seen)
+                if (sp.first == m) {
+                    id = sp.second;
+                    break;
+                }
+            if (id < 0) {
+                id = (int)v3m.size();
+                seen.push_back({m, id});
+                v3m.emplace_back();
+                if (!v3_encode_map(state, n, (uint64_t)nslots, m, &v3m.back()))
+                    return fail(QT_ECUDA, "tile_pass_v3: cuTensorMapEncodeTiled failed for a tile layout");
+            }
+            h_sl[k].pad = id;
+        }
+    }
     // device buffers
     QT_CK(B.pass_start.ensure(sizeof(int32_t) * nslots));
     QT_CK(B.pass_count.ensure(sizeof(int32_t) * nslots));
@@ -404,6 +427,11 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
     if ((e = h2d(B.records, L.records, sizeof(int32_t) * (size_t)nslots * P.n_recorded)) != QT_OK) return e;
     if ((e = h2d(B.traj_ids, L.traj_ids, sizeof(uint64_t) * nslots)) != QT_OK) return e;
     if ((e = h2d(B.slot_list, L.slot_list, sizeof(PassDesc) * step_off[maxp])) != QT_OK) return e;
+    if (!v3m.empty()) {
+        QT_CK(B.maps.ensure(sizeof(V3Map) * v3m.size()));
+        QT_CK(cudaMemcpyAsync(B.maps.p, v3m.data(), sizeof(V3Map) * v3m.size(), cudaMemcpyHostToDevice, ps));
+        QT_CK(cudaStreamSynchronize(ps));  // v3m is a local
+    }
     QT_CK(cudaMemsetAsync(B.status.p, 0, sizeof(int32_t) * nslots, ps));
     QT_CK(cudaMemsetAsync(B.counters.p, 0, sizeof(int32_t) * nslots, ps));
     QT_CK(launch_materialize(B.fused.as<FusedDesc>(), (int)nf, P.tc ? P.tc_k : P.R, B.cons.as<ConsDesc>(),
@@ -435,6 +463,7 @@ qt_status launch_batch(qt_ctx ctx, const Plan& P, std::vector<TrajProgram>& prog
     A.obs_part = B.obs_part.as<double>();
     A.n_obs = n_obs;
     A.obs = ctx->obs.as<ObsDesc>();
+    A.v3maps = P.v3 ? B.maps.p : nullptr;
     for (int step = 0; step < maxp; ++step) {
         const int act = step_off[step + 1] - step_off[step];
         A.step_passes = B.slot_list.as<PassDesc>() + step_off[step];
@@ -735,6 +764,7 @@ static qt_status run_single(qt_ctx ctx, qt_plan plan, float2* state, const ObsGr
                             uint64_t traj, uint64_t* out_bits, double* out_obs, int repeats, double* kernel_ms,
                             bool zero_state, const SingleExtras* ex = nullptr) {
     const Plan& P = plan_of(plan);
+    if (P.v3) return fail(QT_EINVAL, "plans with tile_bits = 11 run through qt_run_trajectories only");
     QT_CK(cudaSetDevice(ctx->device));
     qt_status e = upload_plan_tables(ctx, P, obs_table);
     if (e != QT_OK) return e;
@@ -912,7 +942,7 @@ qt_status qt_plan_info(qt_plan plan, uint64_t seed, uint64_t traj, int64_t* out)
     out[6] = (int64_t)pg.alg_bytes;
     out[7] = (int64_t)pg.cons.size();
     out[8] = P.T;
-    out[9] = P.v2 ? 13 : (P.tc ? P.tc_k : 0);
+    out[9] = P.v3 ? 11 : (P.v2 ? 13 : (P.tc ? P.tc_k : 0));
     return QT_OK;
 }
 

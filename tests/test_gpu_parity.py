@@ -460,3 +460,26 @@ def test_calibrated_qcs_noise_model_parity(ctx):
     noisy.observables = ["Z" + "I" * (c.n_qubits - 1), "I" * (c.n_qubits - 1) + "Z"]
     ref, out, state = run_both(ctx, noisy, seed=77, T=32)
     assert compare(ref, out, state) == 0
+
+
+# ---------------------------------------------------------------------------
+# Experimental TMA-pipelined kernel on 11-qubit tiles (tile_pass_v3.cu, tile_bits = 11)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("case", ["unitary", "depol", "damping", "c2"])
+def test_tile_pass_v3_matches_oracle(ctx, case):
+    if case == "unitary":
+        c, T = workloads.random_circuit(14, depth=6, seed=3, noise="none"), 4
+    elif case == "depol":
+        c, T = workloads.random_circuit(16, depth=6, seed=4, noise="depol", p=0.02), 6
+    elif case == "damping":
+        c, T = workloads.random_circuit(14, depth=6, seed=5, noise="both", p=0.02, t1_ns=800.0, tphi_ns=1500.0,
+                                        readout=True), 8
+    else:
+        c, T = workloads.sycamore_grid_qcs(config=2), 8
+    ref = oracle.run_trajectories(c, seed=7, traj_count=T, shots=2, want_states=True)
+    plan = qtraj.Plan(qtraj.Circuit.from_description(c), max_fused=4, tile_bits=11)
+    assert plan.info(7, 0)["kernel"] == 11
+    state = torch.zeros(T << c.n_qubits, dtype=torch.complex64, device="cuda")
+    out = ctx.run_trajectories(plan, state, seed=7, traj_count=T, shots=2, batch=T, observables=c.observables)
+    torch.cuda.synchronize()
+    compare(ref, out, state)
