@@ -9,6 +9,7 @@
 //           K4 finalize observables, K3 sample bitstrings, download records.
 // While the GPU runs batch i the host plans batch i+1 (two staging slots).
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <array>
@@ -140,6 +141,12 @@ int heap_min_lg() {
     static const int v = getenv("QT_HEAP_MIN_LG") ? atoi(getenv("QT_HEAP_MIN_LG")) : kHeapMinLg;
     return v;
 }
+
+// NVTX range (host timeline of the phases: planning, batch upload / launches, drain)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 template <class F>
 void parallel_for(int count, int threads, F&& fn) {
@@ -636,6 +643,7 @@ void qt_ctx_destroy(qt_ctx ctx) {
 qt_status qt_run_trajectories(qt_ctx ctx, qt_plan plan, const qt_run_opts* opts, int n_obs, const qt_pauli* obs,
                               void* state_dev, size_t state_bytes, uint64_t* out_bits, int32_t* out_kraus,
                               double* out_obs, qt_stats* out_stats) {
+    NvtxRange nvtx_call("qt_run_trajectories");
     if (!ctx || !plan || !opts || !state_dev) return fail(QT_EINVAL, "NULL argument");
     if (n_obs < 0 || (n_obs > 0 && !obs)) return fail(QT_EINVAL, "bad observables");
     if (opts->mode != 0 && opts->mode != 1) return fail(QT_EINVAL, "mode must be 0 (delayed) or 1 (conventional)");
@@ -697,16 +705,23 @@ qt_status qt_run_trajectories(qt_ctx ctx, qt_plan plan, const qt_run_opts* opts,
         for (int b = 0; b < ns; ++b) trajs[b] = opts->traj_begin + (j0 + b) * stride;
         std::vector<qt_status> pst(ns, QT_OK);
         const auto h0 = std::chrono::steady_clock::now();
-        parallel_for(ns, threads,
-                     [&](int b) { pst[b] = plan_trajectory(P, opts->seed, trajs[b], og, progs[b], opts->mode); });
+        {
+            NvtxRange r("qt: plan batch (Alg. 2 first loop + fuser)");
+            parallel_for(ns, threads,
+                         [&](int b) { pst[b] = plan_trajectory(P, opts->seed, trajs[b], og, progs[b], opts->mode); });
+        }
         plan_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
         for (int b = 0; b < ns; ++b)
             if (pst[b] != QT_OK) status = pst[b];
         if (status != QT_OK) break;
         BatchBufs& B = ctx->bb[which];
         // the slot's previous batch must be finished before its buffers are reused
-        if ((status = finish_batch(B, P, shots, n_obs, out)) != QT_OK) break;
+        {
+            NvtxRange r("qt: drain previous batch");
+            if ((status = finish_batch(B, P, shots, n_obs, out)) != QT_OK) break;
+        }
         B.j0 = j0;
+        NvtxRange r("qt: upload + launch batch");
         status = launch_batch(ctx, P, progs, trajs, B, state, shots, opts->seed, n_obs, n_obs > 0, shots > 0, 1, &st,
                               opts->profile != 0);
         which ^= 1;
@@ -882,6 +897,7 @@ static qt_status run_single(qt_ctx ctx, qt_plan plan, float2* state, const ObsGr
 
 qt_status qt_apply_gate_ex(qt_ctx ctx, void* state_dev, int n, int nq, const int* qubits, const double* U,
                            int repeats, double* kernel_ms) {
+    NvtxRange nvtx_call("qt_apply_gate");
     if (!ctx || !state_dev) return fail(QT_EINVAL, "NULL argument");
     qt_circuit c = nullptr;
     qt_status e = qt_circuit_create(n, &c);
