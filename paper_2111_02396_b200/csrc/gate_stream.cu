@@ -57,7 +57,11 @@ struct Cfg {
     // STAGES is a multiple of NWG: stage s is always computed by warpgroup s % NWG, so
     // every barrier of a stage is waited on in phase order (a waiter two phases ahead of
     // a barrier would see the parity of an old phase and pass)
-    static constexpr int NWG = K == 6 ? 2 : (K == 5 ? 3 : 4);
+    // K = 6: one warpgroup of 256 threads, two per row (configurations 0..31 / 32..63), so
+    // that one of the two 64 KB stages is free for loads while the other computes
+    static constexpr int SPLIT = K == 6 ? 2 : 1;      // threads per row
+    static constexpr int WGT = 128 * SPLIT;            // threads per compute warpgroup
+    static constexpr int NWG = K == 6 ? 1 : (K == 5 ? 3 : 4);
     static constexpr uint32_t TILE_BYTES = 128u * CFG * 8u;
     static constexpr int STAGES = K == 4 ? 12 : (K == 5 ? 6 : 2);
     static constexpr int STORE_LAG = STAGES >= 6 ? 1 : 0;
@@ -68,8 +72,9 @@ struct Cfg {
     static constexpr int KS = (2 * CFG) / 16;                   // K16 steps per part
     static constexpr uint32_t W_OFF = STAGES * TILE_BYTES;
     static constexpr uint32_t BAR_OFF = W_OFF + W_BYTES;
-    static constexpr uint32_t SMEM = BAR_OFF + 512 + 1024;      // + 1024-byte alignment slack
-    static constexpr int THREADS = NWG * 128 + 64;               // + loader warp + storer warp
+    static constexpr uint32_t AMX_OFF = BAR_OFF + 512;          // SPLIT > 1: per-thread row maxima
+    static constexpr uint32_t SMEM = AMX_OFF + (SPLIT > 1 ? 4 * WGT : 0) + 1024;  // + alignment slack
+    static constexpr int THREADS = NWG * WGT + 64;               // + loader warp + storer warp
     static constexpr int MAXREG = (65536 / THREADS) & ~7;
     static_assert(SMEM <= 232448, "shared memory");
     static_assert(STAGES % NWG == 0, "stage -> warpgroup map");
@@ -128,7 +133,8 @@ __device__ __forceinline__ void tma_store(const CUtensorMap* tm, int32_t crest, 
                  "r"(0), "r"(crest), "r"(src)
                  : "memory");
 }
-__device__ __forceinline__ void bar_wg(int wg) { asm volatile("bar.sync %0, 128;\n" ::"r"(1 + wg) : "memory"); }
+template <int NTH = 128>
+__device__ __forceinline__ void bar_wg(int wg) { asm volatile("bar.sync %0, %1;\n" ::"r"(1 + wg), "n"(NTH) : "memory"); }
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
     asm volatile(
@@ -178,12 +184,12 @@ __global__ void __launch_bounds__(Cfg<K>::THREADS, 1) __maxnreg__(Cfg<K>::MAXREG
 #else
 #define GS_PROG(step)
 #endif
-    const int producer = C::NWG * 128;
+    const int producer = C::NWG * C::WGT;
     if (warp == 0) tc::tmem_alloc(tslot, C::TCOLS);
     if (tid == producer) {
         for (int s = 0; s < C::STAGES; ++s) {
             bar_init(bar + 8u * s, 1);                       // full: producer arrive + TMA bytes
-            bar_init(bar + 8u * (C::STAGES + s), 128);       // computed: the warpgroup's 128 threads
+            bar_init(bar + 8u * (C::STAGES + s), C::WGT);    // computed: the warpgroup's threads
         }
         for (int w = 0; w < C::NWG; ++w) bar_init(bar + 8u * (2 * C::STAGES + w), 1);  // MMA commit
         bar_init(w_bar, 1);
@@ -209,7 +215,7 @@ __global__ void __launch_bounds__(Cfg<K>::THREADS, 1) __maxnreg__(Cfg<K>::MAXREG
         }
         return (int32_t)base;
     };
-    if (warp == C::NWG * 4) {
+    if (warp == C::NWG * C::WGT / 32) {
         // ---------------- loader: TMA loads into free stages ----------------
         if (lane == 0) {
             expect_tx(w_bar, C::W_BYTES);
@@ -227,7 +233,7 @@ __global__ void __launch_bounds__(Cfg<K>::THREADS, 1) __maxnreg__(Cfg<K>::MAXREG
                 for (int o = 0; o < a.nops; ++o) tma_load(st + (uint32_t)o * a.op_bytes, &tm, cr + a.op_rest[o], bar + 8u * s);
             }
         }
-    } else if (warp == C::NWG * 4 + 1) {
+    } else if (warp == C::NWG * C::WGT / 32 + 1) {
         // ---------------- storer: TMA stores of computed tiles, in order ----------------
         // a stage is released once its store has read it; with many stages one store
         // group stays in flight behind the newest (two reads overlap), with two stages
@@ -252,8 +258,10 @@ __global__ void __launch_bounds__(Cfg<K>::THREADS, 1) __maxnreg__(Cfg<K>::MAXREG
         }
     } else {
         // ---------------- compute warpgroups ----------------
-        const int wg = warp >> 2, wq = warp & 3;
-        const int wtid = tid & 127;
+        constexpr int CPT = CFG / C::SPLIT;  // configurations per thread
+        const int wg = warp / (4 * C::SPLIT), wq = warp & 3, hsel = (warp >> 2) & (C::SPLIT - 1);
+        const int wtid = tid % C::WGT;
+        const int cbase = hsel * CPT;  // this thread's first configuration
         const uint32_t tl = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)wg * C::COLS;  // lane, D column 0
         const uint32_t tA = tl + (uint32_t)C::N;                                          // A: hi, then lo
         uint32_t ro = 0;
@@ -287,7 +295,7 @@ __global__ void __launch_bounds__(Cfg<K>::THREADS, 1) __maxnreg__(Cfg<K>::MAXREG
             // (experiment: a.reps > 1 applies the gate reps times per tile -- the cost of
             // several gates per HBM pass in this pipeline; tools/gs_reps.py)
             for (int rep = 0; rep < a.reps; ++rep) {
-            if (rep) bar_wg(wg);  // the previous application's write-backs are visible
+            if (rep) bar_wg<C::WGT>(wg);  // the previous application's write-backs are visible
             // ---- gather the row's 2^K amplitudes, per-row power-of-two scale ----
             auto load16 = [&](int c0, float2 (&v)[16]) {
                 if (pair) {
@@ -304,16 +312,23 @@ __global__ void __launch_bounds__(Cfg<K>::THREADS, 1) __maxnreg__(Cfg<K>::MAXREG
             };
             // K >= 5: two passes over the tile (amax, then split) so that 32 / 64 amplitudes
             // need not stay in registers; K = 4: one pass
-            constexpr int NCH = CFG / 16;
-            constexpr int KEEP = K >= 5 ? 1 : NCH;
+            constexpr int NCH = CPT / 16;
+            constexpr int KEEP = (K == 5) ? 1 : NCH;
             float2 v[KEEP][16];
             float amax = 0.f;
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch) {
                 float2(&w)[16] = v[KEEP == 1 ? 0 : ch];
-                load16(16 * ch, w);
+                load16(cbase + 16 * ch, w);
 #pragma unroll
                 for (int c = 0; c < 16; ++c) amax = fmaxf(amax, fmaxf(fabsf(w[c].x), fabsf(w[c].y)));
+            }
+            if constexpr (C::SPLIT > 1) {
+                // the row's other half: thread wtid ^ 128 (same lane quarter, other warp half)
+                float* amx = reinterpret_cast<float*>(sm + C::AMX_OFF);
+                amx[wtid] = amax;
+                bar_wg<C::WGT>(wg);
+                amax = fmaxf(amax, amx[wtid ^ 128]);
             }
             // amax * 2^(se - 127) in [2^6, 2^7): |A| < 2^7, row outputs < 2^7 * 2^(K/2) * ||U||
             int se = 260 - (int)((__float_as_uint(amax) >> 23) & 0xffu);
@@ -323,18 +338,18 @@ __global__ void __launch_bounds__(Cfg<K>::THREADS, 1) __maxnreg__(Cfg<K>::MAXREG
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch) {
                 float2(&w)[16] = v[KEEP == 1 ? 0 : ch];
-                if (KEEP == 1) load16(16 * ch, w);
+                if (KEEP == 1) load16(cbase + 16 * ch, w);
                 uint32_t hi[16], lo[16];
 #pragma unroll
                 for (int c = 0; c < 16; ++c) split2(w[c].x * scale, w[c].y * scale, hi[c], lo[c]);
-                tmem_st16(tA + (uint32_t)(16 * ch), hi);
-                tmem_st16(tA + (uint32_t)(CFG + 16 * ch), lo);
+                tmem_st16(tA + (uint32_t)(cbase + 16 * ch), hi);
+                tmem_st16(tA + (uint32_t)(CFG + cbase + 16 * ch), lo);
             }
             GS_PROG(3);
             tc::tmem_wait_st();
             GS_PROG(4);
             tc::fence_before();
-            bar_wg(wg);  // A complete; every read of the tile done
+            bar_wg<C::WGT>(wg);  // A complete; every read of the tile done
             GS_PROG(5);
             if (wtid == 0) {
                 tc::fence_after();
@@ -364,7 +379,8 @@ __global__ void __launch_bounds__(Cfg<K>::THREADS, 1) __maxnreg__(Cfg<K>::MAXREG
             tc::fence_after();
             // ---- D row -> amplitudes (unscaled) -> tile, in place ----
 #pragma unroll
-            for (int c0 = 0; c0 < CFG; c0 += 16) {
+            for (int cc = 0; cc < CPT; cc += 16) {
+                const int c0 = cbase + cc;
                 uint32_t d[32];
                 tc::tmem_ld32(tl + 2u * (uint32_t)c0, d);
                 tc::tmem_wait_ld();
