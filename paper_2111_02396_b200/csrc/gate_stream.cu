@@ -482,7 +482,10 @@ static void f16_split(double x, uint16_t& hi, uint16_t& lo) {
 // m-th lowest qubit, row-major 2^nq x 2^nq).  false if the register is too small
 // (n < 7 + K) or the tensor map cannot be encoded.
 static bool plan_gate(void* state, int n, int nq, const int* qs, const cd* U, GsPlan& P) {
-    const int K = std::max(nq, 4);
+    // k <= 4 gates run padded to 5 qubits when the register allows: the 32 KB tiles of the
+    // K = 5 kernel stream at 0.94 - 0.96 of HBM for every placement, the 16 KB K = 4 tiles at
+    // 0.86 - 0.94 (twice the boxes and barrier round trips per byte)
+    const int K = std::max(nq, n >= 12 ? 5 : 4);
     if (n < 7 + K) return false;
     P.K = K;
     // matrix qubits: the gate's plus the lowest free ones as padding
