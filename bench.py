@@ -192,7 +192,7 @@ def gate_pass_sweep(ctx, n, dev, hbm_peak, reps=10):
     return {"n": n, "bytes_per_pass": 2 ** (n + 4), "peak_gbs": hbm_peak, "best_gbs": best, "median_gbs": med,
             "best_frac": best / hbm_peak, "median_frac": med / hbm_peak,
             "min_frac": min(r["frac"] for r in rows),
-            "kernel": "gate_stream_kernel<K> (qt_apply_gate: TMA tensor-map tiles, tcgen05 f16 hi/lo GEMM, K = max(k, 4))",
+            "kernel": "gate_stream_kernel<K> (qt_apply_gate: TMA tensor-map tiles, tcgen05 f16 hi/lo GEMM, K = max(k, 5) on n >= 12)",
             "k4_median_frac": float(np.median([r["frac"] for r in rows if r["k"] <= 4])), "rows": rows}
 
 
