@@ -116,3 +116,18 @@ def test_stream_single_cta_ring(ctx):
             assert rel_l2(run(ctx, psi, qs, U), ref) < AMP_TOL, qs
     finally:
         del os.environ["QT_GS_GRID"]
+
+
+@pytest.mark.parametrize("n", [11, 12, 13])
+def test_stream_register_size_boundaries(ctx, n):
+    """Smallest registers of each tile shape: n = 11 runs k <= 4 on the K = 4 kernel (one
+    2^11 tile), n = 12 pads k <= 4 to K = 5 (one 2^12 tile), n = 13 admits K = 6; larger gates
+    than the register allows fall back to the trajectory kernels."""
+    rng = np.random.default_rng(200 + n)
+    for k in range(1, 7):
+        for qs in (list(range(k)), list(range(n - k, n)),
+                   sorted(int(x) for x in rng.choice(n, size=k, replace=False))):
+            U = workloads.haar_unitary(rng, 2 ** k)
+            psi = rand_state(rng, n)
+            ref = oracle.apply_gate(psi.copy(), qs, U)
+            assert rel_l2(run(ctx, psi, qs, U), ref) < AMP_TOL, (n, qs)
