@@ -652,16 +652,19 @@ static bool plan_gate(void* state, int n, int nq, const int* qs, const cd* U, Gs
 template <int K>
 static cudaError_t launch_k(const GsPlan& P, const void* w_dev, cudaStream_t s) {
     using C = Cfg<K>;
-    static bool configured = false;
-    static int sms = 0;
-    if (!configured) {
+    // kernel attribute and SM count per device (contexts may live on different GPUs)
+    static int sms_of[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    int& sms = sms_of[dev];
+    if (!sms) {
         cudaError_t e = cudaFuncSetAttribute(gate_stream_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)C::SMEM);
         if (e != cudaSuccess) return e;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        configured = true;
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        sms = n;
     }
     uint32_t grid = std::min<uint32_t>(P.a.ntiles, (uint32_t)sms);
     if (const char* g = getenv("QT_GS_GRID")) grid = std::min<uint32_t>(grid, (uint32_t)std::max(1, atoi(g)));
@@ -679,12 +682,17 @@ cudaError_t gate_stream_apply(cudaStream_t s, void* state, int n, int nq, const 
                               int repeats, double* kernel_ms) {
     gs::GsPlan P;
     if (!gs::plan_gate(state, n, nq, qs, U, P)) return cudaErrorNotSupported;
-    static void* w_dev = nullptr;
-    if (!w_dev) {
-        cudaError_t e = cudaMalloc(&w_dev, 65536);
-        if (e != cudaSuccess) return e;
-    }
-    cudaError_t e = cudaMemcpyAsync(w_dev, P.w.data(), P.w.size() * 2, cudaMemcpyHostToDevice, s);
+    // the W operand lives in a stream-ordered allocation of this call (no state shared
+    // between contexts, devices or threads)
+    void* w_dev = nullptr;
+    cudaError_t e = cudaMallocAsync(&w_dev, P.w.size() * 2, s);
+    if (e != cudaSuccess) return e;
+    struct Free {
+        void* p;
+        cudaStream_t s;
+        ~Free() { cudaFreeAsync(p, s); }
+    } w_free{w_dev, s};
+    e = cudaMemcpyAsync(w_dev, P.w.data(), P.w.size() * 2, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // P.w is a local
     if (e != cudaSuccess) return e;
     auto one = [&]() {
