@@ -85,9 +85,11 @@ def main():
                                       want_states=True)
         res["oracle_s"] = time.time() - t0
         assert ref["rc"] == 0
-        for tile_bits in (0, 13):
+        # per-tile kernel (12-qubit tiles), persistent TMEM kernel (13, the default), the
+        # experimental TMA-pipelined kernel (11); the last full run is the default's
+        for tile_bits in (12, 11, 13):
             out, psi = gpu_run(c, seed, begin, stride, count, 4, count, tile_bits)
-            res[f"gpu_f4_tile{tile_bits or 12}"] = compare(ref, out, psi)
+            res[f"gpu_f4_tile{tile_bits}"] = compare(ref, out, psi)
         # batch invariance: the same indices inside the full bench job (batch 384)
         ctx = qtraj.Context(0)
         plan = qtraj.Plan(qtraj.Circuit.from_description(c), max_fused=4)
@@ -108,6 +110,8 @@ def main():
         for f in (4, 6):
             out, psi = gpu_run(c, seed, 0, 1, 2, f, 2)
             res[f"gpu_f{f}"] = compare(ref, out, psi)
+        out, psi = gpu_run(c, seed, 0, 1, 2, 4, 2, 11)
+        res["gpu_f4_tile11"] = compare(ref, out, psi)
     print(json.dumps(res))
     if a.out:
         with open(a.out, "w") as fh:
