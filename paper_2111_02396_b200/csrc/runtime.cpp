@@ -665,6 +665,9 @@ qt_status qt_run_trajectories(qt_ctx ctx, qt_plan plan, const qt_run_opts* opts,
     int batch = opts->batch > 0 ? opts->batch : 256;
     batch = (int)std::min<size_t>((size_t)batch, max_slots);
     batch = std::min(batch, 65535);
+    // T = 11 (tile_pass_v3.cu): TMA rest coordinates are int32 units of 16 amplitudes over
+    // the whole batch buffer
+    if (P.v3) batch = (int)std::min<int64_t>((int64_t)batch, std::max<int64_t>(1, (int64_t(1) << 31) >> (P.n - 4)));
     const uint64_t stride = opts->traj_stride ? opts->traj_stride : 1;
     const int shots = opts->shots_per_traj;
     int threads = opts->host_threads > 0 ? opts->host_threads : (int)std::thread::hardware_concurrency();

@@ -747,6 +747,7 @@ bool v3_encode_map(void* state, int n, uint64_t nslots, uint64_t tile_mask, V3Ma
             fn = reinterpret_cast<EncodeTiledFnV3>(p);
     }
     if (!fn || (tile_mask & 15ull) != 15ull || __builtin_popcountll(tile_mask) != v3::T) return false;
+    if (n - 4 > 31 || (nslots << (n - 4)) > 0x7fffffffull) return false;  // int32 rest coordinates
     int runs_q[16], runs_len[16], nr = 0;
     for (int q = 4; q < n;) {
         if (!((tile_mask >> q) & 1ull)) {
