@@ -139,7 +139,9 @@ typedef struct {
     int max_fused;    /* f in [2, 6]; 0 = 4 */
     int tile_bits;    /* qubits held per tile; 0 = auto: 13 for n >= 13 with 4-qubit tensor-core
                          gates (persistent TMEM kernel), else 12, or n if n < 12; 12 forces the
-                         per-tile kernel */
+                         per-tile kernel; 11 (n >= 12, max_fused <= 4) selects the experimental
+                         TMA-pipelined kernel (plans run through qt_run_trajectories only;
+                         QT_EINVAL from the stand-alone calls) */
     int low_bits;     /* lowest qubits always in a tile (coalescing); 0 = auto (4) */
     int one_gate_per_pass; /* 1 = every fused gate is its own HBM pass (the paper's GPU scheme) */
     int tensor_cores;      /* 0 = auto (on when n >= 12; fused gates padded to max(f, 4) qubits),
@@ -191,7 +193,10 @@ qt_status qt_run_trajectories(qt_ctx ctx, qt_plan plan, const qt_run_opts* opts,
                               qt_stats* out_stats);
 
 /* ---- stand-alone state operations -----------------------------------------
- * qt_apply_gate: Alg. 1 for one gate on a caller state (in place).
+ * qt_apply_gate: Alg. 1 for one gate on a caller state (in place):
+ *   one HBM pass of the streaming kernel (TMA tiles of 128 rows x 2^K amplitudes,
+ *   K = max(nq, 5) for n >= 12, max(nq, 4) for n = 11; smaller registers, or gates
+ *   wider than the register's tiles allow, run on the trajectory kernels).
  * qt_sample_bitstrings: chain-rule sampling (most significant qubit first)
  *   of `shots` bitstrings from |psi|^2 (norm-invariant), trajectory index
  *   `traj` selects the RNG stream; no readout error is applied.
