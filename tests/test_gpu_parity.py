@@ -483,3 +483,23 @@ def test_tile_pass_v3_matches_oracle(ctx, case):
     out = ctx.run_trajectories(plan, state, seed=7, traj_count=T, shots=2, batch=T, observables=c.observables)
     torch.cuda.synchronize()
     compare(ref, out, state)
+
+
+def test_tile_pass_v3_measurement_and_readout(ctx):
+    """tile_bits = 11 with mid-circuit measurements (projector channels, always the
+    conventional branch: rho_Q epilogue + device choice) and readout error."""
+    n, T = 14, 12
+    rng = np.random.default_rng(41)
+    c = workloads.random_circuit(n, depth=6, seed=41, max_arity=2, noise="depol", readout=True)
+    moms = []
+    for i, m in enumerate(c.moments):
+        moms.append(m)
+        if i % 3 == 2:
+            moms.append([workloads.measurement(int(q)) for q in rng.choice(n, 2, replace=False)])
+    c.moments = moms
+    ref = oracle.run_trajectories(c, seed=9, traj_count=T, shots=3, want_states=True)
+    plan = qtraj.Plan(qtraj.Circuit.from_description(c), max_fused=4, tile_bits=11)
+    state = torch.zeros(T << n, dtype=torch.complex64, device="cuda")
+    out = ctx.run_trajectories(plan, state, seed=9, traj_count=T, shots=3, batch=T, observables=c.observables)
+    torch.cuda.synchronize()
+    assert compare(ref, out, state) == 0
