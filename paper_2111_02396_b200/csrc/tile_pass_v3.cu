@@ -308,28 +308,31 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == NWG * 4) {
         // ---------------- loader ----------------
-        if (lane == 0) {
-            for (uint32_t j = 0; j < my_items; ++j) {
-                const int s = (int)(j % STAGES);
-                if (j + 4 < my_items) pf_l1(A.step_passes + (raw(j + 4) >> tshift));  // descriptors ahead
+        // the whole warp: lane 0 waits for the stage and posts the expected bytes, lane o
+        // issues box o (a tile of scattered qubits takes up to 16 boxes)
+        for (uint32_t j = 0; j < my_items; ++j) {
+            const int s = (int)(j % STAGES);
+            if (lane == 0 && j + 4 < my_items) pf_l1(A.step_passes + (raw(j + 4) >> tshift));  // descriptors ahead
 #ifdef QT_V3_TIMING
-                long long tt = clock64();
+            long long tt = clock64();
 #endif
-                if (j >= (uint32_t)STAGES) wait(empty_b(s), ((j / STAGES) - 1u) & 1u);
-                V3T(10, tt);
-                const uint32_t i = raw(j);
-                const PassDesc P = A.step_passes[i >> tshift];
-                if (P.flags & kPassInit) {
-                    arrive(full_b(s));  // the warpgroup builds |0...0> in place
-                    continue;
-                }
-                const V3Map* M = maps + P.pad;
-                expect_tx(full_b(s), kTileBytes);
-                const int32_t cr = crest_of(P, i & (ntiles - 1u));
-                const uint32_t st = sm_s + (uint32_t)s * kTileBytes;
-                for (int o = 0; o < M->nops; ++o) tma_load(st + (uint32_t)o * M->op_bytes, &M->tm, cr + M->op_rest[o], full_b(s));
-                V3T(11, tt);
+            if (j >= (uint32_t)STAGES) wait(empty_b(s), ((j / STAGES) - 1u) & 1u);
+            __syncwarp();
+            if (lane == 0) { V3T(10, tt); }
+            const uint32_t i = raw(j);
+            const PassDesc P = A.step_passes[i >> tshift];
+            if (P.flags & kPassInit) {
+                if (lane == 0) arrive(full_b(s));  // the warpgroup builds |0...0> in place
+                continue;
             }
+            const V3Map* M = maps + P.pad;
+            if (lane == 0) expect_tx(full_b(s), kTileBytes);
+            __syncwarp();
+            const int32_t cr = crest_of(P, i & (ntiles - 1u));
+            const uint32_t st = sm_s + (uint32_t)s * kTileBytes;
+            const int nops = M->nops;
+            if (lane < nops) tma_load(st + (uint32_t)lane * M->op_bytes, &M->tm, cr + M->op_rest[lane], full_b(s));
+            if (lane == 0) { V3T(11, tt); }
         }
     } else if (warp == NWG * 4 + 1) {
         // ---------------- storer ----------------
