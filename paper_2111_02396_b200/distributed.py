@@ -35,6 +35,8 @@ from __future__ import annotations
 
 from typing import Dict, List, Optional, Sequence
 
+import os
+
 import numpy as np
 
 from . import qtraj
@@ -62,11 +64,16 @@ class GpuBackend:
         return s
 
     def apply_ops(self, state, n_local: int, ops):
-        c = qtraj.Circuit(n_local)
-        for i, (pos, M) in enumerate(ops):
-            c.add_matrix(i, pos, M)
-        plan = qtraj.Plan(c, max_fused=max(self.max_fused, max(len(p) for p, _ in ops)))
-        self.ctx.apply_plan(plan, state)
+        # the chunks of one exchange share their operation list: one plan for all of them
+        key = (id(ops), n_local)
+        if getattr(self, "_plan_key", None) != key:
+            c = qtraj.Circuit(n_local)
+            for i, (pos, M) in enumerate(ops):
+                c.add_matrix(i, pos, M)
+            self._plan = qtraj.Plan(c, max_fused=max(self.max_fused, max(len(p) for p, _ in ops)))
+            self._plan_key = key
+            self._plan_ops = ops  # keeps id(ops) from being reused while cached
+        self.ctx.apply_plan(self._plan, state)
 
     def permute(self, state, perm):
         # ping-pong with one spare buffer per size: a 33-qubit slice (64 GiB)
@@ -118,9 +125,10 @@ class EmulatedFabric:
         self.world = world
         self.local_ranks = list(range(world))
 
-    def exchange_top(self, states: Dict[int, object], gbits: Sequence[int], s: int, pool=None):
+    def exchange_top(self, states: Dict[int, object], gbits: Sequence[int], s: int, pool=None, on_chunk=None):
         """Swap the top s local bits with global bits gbits (top local bit
-        n_local - s + j <-> rank bit gbits[j])."""
+        n_local - s + j <-> rank bit gbits[j]).  on_chunk(rank, view), if given, is
+        called once per received chunk (a contiguous 2^(n_local - s) block)."""
         out = {}
         size = states[0].numel()
         chunk = size >> s
@@ -131,6 +139,8 @@ class EmulatedFabric:
                 d = _dest(r, gbits, c)
                 cp = _src_chunk(r, gbits)
                 out[d][cp * chunk:(cp + 1) * chunk].copy_(states[r][c * chunk:(c + 1) * chunk])
+                if on_chunk is not None:
+                    on_chunk(d, out[d][cp * chunk:(cp + 1) * chunk])
         return out
 
     def allreduce(self, per_rank: Dict[int, np.ndarray]) -> np.ndarray:
@@ -164,10 +174,12 @@ class TorchFabric:
         # 2-process single-GPU test; NCCL moves device memory directly over NVLink)
         self.stage_host = dist.get_backend(group) == "gloo"
 
-    def exchange_top(self, states, gbits, s, pool=None):
+    def exchange_top(self, states, gbits, s, pool=None, on_chunk=None):
         # chunk c goes to rank _dest(c) and arrives at chunk _src_chunk(source):
         # both are increasing in rank order only for ascending gbits
         assert all(gbits[j] < gbits[j + 1] for j in range(len(gbits) - 1)), "gbits must ascend"
+        if on_chunk is not None:
+            return self._exchange_p2p(states, gbits, s, pool, on_chunk)
         x = states[self.rank]
         chunk = x.numel() >> s
         in_split = [0] * self.world
@@ -186,6 +198,51 @@ class TorchFabric:
             y.copy_(yc)
         else:
             self.dist.all_to_all_single(y, x.contiguous(), out_split, in_split, group=self.group)
+        if hasattr(pool, "give_spare"):
+            pool.give_spare(x)
+        return {self.rank: y}
+
+    def _exchange_p2p(self, states, gbits, s, pool, on_chunk):
+        """The exchange as 2^s - 1 pairwise rounds (round k: the peer whose global-bit
+        value is this rank's XOR k, so partners agree round by round; each round one
+        grouped send + receive), the chunk of round k handed to on_chunk (the deferred
+        local operations) while round k + 1 is in flight; the rank's own chunk first,
+        without communication."""
+        x = states[self.rank].contiguous()
+        chunk = x.numel() >> s
+        y = pool.take_spare(x) if hasattr(pool, "take_spare") else self.torch.empty_like(x)
+        staged = self.stage_host and x.is_cuda
+        xs = x.cpu() if staged else x
+        ys = self.torch.empty_like(xs) if staged else y
+        own = _src_chunk(self.rank, gbits)
+
+        def hand(cp):
+            if staged:
+                y[cp * chunk:(cp + 1) * chunk].copy_(ys[cp * chunk:(cp + 1) * chunk])
+            on_chunk(self.rank, y[cp * chunk:(cp + 1) * chunk])
+
+        ys[own * chunk:(own + 1) * chunk].copy_(xs[own * chunk:(own + 1) * chunk])
+        prev = None
+        for k in range(1, 1 << s):
+            c = own ^ k                       # the chunk that goes to this round's peer
+            peer = _dest(self.rank, gbits, c)
+            cp = _src_chunk(peer, gbits)      # where the peer's chunk lands (= c)
+            works = self.dist.batch_isend_irecv([
+                self.dist.P2POp(self.dist.isend, xs[c * chunk:(c + 1) * chunk], peer, self.group),
+                self.dist.P2POp(self.dist.irecv, ys[cp * chunk:(cp + 1) * chunk], peer, self.group)])
+            if prev is None:
+                hand(own)  # overlaps the first round
+            else:
+                for w in prev[0]:
+                    w.wait()
+                hand(prev[1])
+            prev = (works, cp)
+        if prev is None:
+            hand(own)
+        else:
+            for w in prev[0]:
+                w.wait()
+            hand(prev[1])
         if hasattr(pool, "give_spare"):
             pool.give_spare(x)
         return {self.rank: y}
@@ -247,6 +304,9 @@ class DistributedTrajectory:
         self.rank_ops = {r: [] for r in fabric.local_ranks}
         self.swaps = 0
         self.exchanged_bytes = 0
+        # pending local operations that commute with a swap run per received chunk
+        self.overlap = os.environ.get("QT_DIST_OVERLAP", "1") != "0"
+        self.deferred_ops = 0
 
     # -- helpers ------------------------------------------------------------
     def _flush(self):
@@ -261,6 +321,28 @@ class DistributedTrajectory:
         self.pending_all = []
         self.rank_ops = {r: [] for r in self.f.local_ranks}
 
+    def _split_pending(self, vslots: set) -> List:
+        """Remove from the pending lists the shared operations that can follow the
+        exchange and return them (positions, matrix) in program order: an operation must
+        stay before it if it touches a victim slot, is rank-specific (its rank-independent
+        marker keeps its slots), or shares a slot with a later operation that stays
+        (reverse scan); the decision uses only state shared by every rank, because the
+        deferred operations are applied to chunks that arrive from other ranks."""
+        keep = [False] * len(self.pending_all)
+        need = set(vslots)
+        for i in range(len(self.pending_all) - 1, -1, -1):
+            tag, pos, _ = self.pending_all[i]
+            if tag >= 0:
+                keep[i] = True  # rank-specific: decided by its marker, identically on every rank
+            elif tag == -2 or any(p in need for p in pos):
+                keep[i] = True
+                need.update(pos)
+        after = [(pos, M) for (tag, pos, M), k in zip(self.pending_all, keep) if not k]
+        if after:
+            self.pending_all = [o for o, k in zip(self.pending_all, keep) if k]
+            self.pending = [(pos, M) for tag, pos, M in self.pending_all if tag == -1]
+        return after
+
     def _push(self, pos, M):
         self.pending.append((pos, M))
         self.pending_all.append((-1, pos, M))
@@ -272,6 +354,9 @@ class DistributedTrajectory:
         (qt_restrict_diagonal)."""
         d = np.diag(np.asarray(M, np.complex128))
         loc = [m for m, q in enumerate(qubits) if self.slot[q] < self.nl]
+        # rank-independent marker (every rank records it): the slots a later exchange must
+        # not defer past; the per-rank entries below differ between ranks
+        self.pending_all.append((-2, [self.slot[qubits[m]] for m in loc], None))
         for r in self.f.local_ranks:
             fixed = [(r >> (self.slot[q] - self.nl)) & 1 if self.slot[q] >= self.nl else -1 for q in qubits]
             dd, k = qtraj.restrict_diagonal(d, fixed)
@@ -318,6 +403,10 @@ class DistributedTrajectory:
         pairs = sorted(zip(glob, victims), key=lambda gv: self.slot[gv[0]])
         glob = [g for g, _ in pairs]
         victims = [v for _, v in pairs]
+        # pending operations that touch no victim (and precede no operation that must be
+        # applied first) commute with the exchange: they are applied to every received
+        # chunk, overlapping the transfers of the others; the rest is flushed now
+        after = self._split_pending({self.slot[v] for v in victims}) if self.overlap else []
         self._flush()
         # local permutation: victim j -> top slot nl - s + j (swapping with the occupant)
         top = [self.nl - s + j for j in range(s)]
@@ -330,10 +419,18 @@ class DistributedTrajectory:
             w = occupant[b]
             occupant[a], occupant[b] = w, v
             cur[v], cur[w] = b, a
-        self._apply_local_perm({self.slot[q]: cur[q] for q in range(self.n)
-                                if self.slot[q] < self.nl and cur[q] != self.slot[q]})
+        moved = {self.slot[q]: cur[q] for q in range(self.n) if self.slot[q] < self.nl and cur[q] != self.slot[q]}
+        self._apply_local_perm(moved)
         gbits = [self.slot[q] - self.nl for q in glob]
-        self.states = self.f.exchange_top(self.states, gbits, s, pool=self.b)
+        if after:
+            # positions through the local permutation; none is a top (victim) slot
+            ops = [([moved.get(p, p) for p in pos], M) for pos, M in after]
+            assert all(p < self.nl - s for pos, _ in ops for p in pos)
+            self.deferred_ops += len(ops)
+            self.states = self.f.exchange_top(self.states, gbits, s, pool=self.b,
+                                              on_chunk=lambda r, view: self.b.apply_ops(view, self.nl - s, ops))
+        else:
+            self.states = self.f.exchange_top(self.states, gbits, s, pool=self.b)
         self.swaps += 1
         self.exchanged_bytes += (1 - 2.0 ** -s) * 8 * (1 << self.nl) * len(self.f.local_ranks)
         for j, q in enumerate(glob):

@@ -265,3 +265,25 @@ def test_gpu_backend_torch_fabric_two_processes():
             bad = [s for s in range(3) if out["bits"][s] != ref["bits"][t][s] and ref["sample_margin"][t][s] >= 1e-4]
             assert not bad
             assert np.max(np.abs(out["obs"] - ref["obs"][t])) < 1e-4
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_overlapped_exchange_defers_and_matches(world):
+    """Pending local operations that commute with a swap are applied per received chunk
+    (overlapping the exchange); the result equals the flush-everything-first schedule and
+    the oracle, and some operations were actually deferred."""
+    n = 8
+    c = circuit(n, seed=9)
+    seed = 55
+    ref = oracle.run_trajectories(c, seed=seed, traj_count=1, shots=2)
+    outs = {}
+    for ov in (False, True):
+        tr = D.DistributedTrajectory(NumpyBackend(), D.EmulatedFabric(world), n)
+        tr.overlap = ov
+        outs[ov] = tr.run(c, seed=seed, traj=0, shots=2, observables=c.observables)
+        if ov:
+            assert tr.deferred_ops > 0
+    check(outs[True], ref, 0)
+    assert (outs[True]["kraus"] == outs[False]["kraus"]).all()
+    assert (outs[True]["bits"] == outs[False]["bits"]).all()
+    assert np.max(np.abs(np.asarray(outs[True]["obs"]) - np.asarray(outs[False]["obs"]))) < 1e-10

@@ -96,8 +96,18 @@ class DryFabric:
     def __init__(self, world):
         self.world = world
         self.local_ranks = list(range(world))
+        self.exchanges = []
 
-    def exchange_top(self, states, gbits, s, pool=None):
+    def exchange_top(self, states, gbits, s, pool=None, on_chunk=None):
+        # per exchange: s and the tile passes per rank of the operations deferred into it
+        # (applied per received chunk while the other chunks are in flight); priced once per
+        # rank on its whole slice, the same bytes as per chunk
+        before = pool.passes if pool is not None else 0
+        if on_chunk is not None:
+            for r, st in states.items():
+                on_chunk(r, st)
+        deferred = (pool.passes - before) / self.world if pool is not None else 0.0
+        self.exchanges.append((s, deferred))
         return dict(states)
 
     def allreduce(self, per_rank):
@@ -142,22 +152,39 @@ def main():
     for gamma in sorted({0.0, a.gamma}):
         c = c5_circuit(n, a.cycles, gamma)
         b = DryBackend()
-        tr = D.DistributedTrajectory(b, DryFabric(a.world), n)
+        fab = DryFabric(a.world)
+        tr = D.DistributedTrajectory(b, fab, n)
         res = tr.run(c, seed=workloads.trajectory_seed(5), traj=0, shots=1)
         per_rank_bytes = tr.exchanged_bytes / a.world
         state_b = 8.0 * (1 << nl)
-        t_pass = b.passes * 2 * state_b / rate
+        deferred_passes = sum(d for _, d in fab.exchanges)
+        t_pass = (b.passes - deferred_passes * a.world) * 2 * state_b / rate
         t_perm = b.permutes / a.world * 2 * state_b / rate
         t_red = b.reductions / a.world * state_b / rate
         t_x = per_rank_bytes / (a.nvlink_gbs * 1e9)
+        # exchange phases: 2^s - 1 pairwise rounds; the deferred passes run per received
+        # chunk (own chunk during round 1), so a phase takes
+        # R max(x / R, p / 2^s) + p / 2^s for transfer time x and deferred pass time p
+        t_xphase, t_xphase_serial = 0.0, 0.0
+        for sk, dk in fab.exchanges:
+            xk = (1 - 2.0 ** -sk) * state_b / (a.nvlink_gbs * 1e9)
+            pk = dk * 2 * state_b / rate
+            rr = (1 << sk) - 1
+            t_xphase += rr * max(xk / rr, pk / (1 << sk)) + pk / (1 << sk)
+            t_xphase_serial += xk + pk
         key = "noiseless" if gamma == 0 else f"amplitude_damping_{gamma:g}"
         out[key] = {
             "ops": sum(1 for _ in c.ops()), "swaps": int(res["swaps"]), "bytes_sent_per_rank": per_rank_bytes,
             "local_permutations_per_rank": b.permutes / a.world, "flushes": b.flushes / a.world,
             "tile_passes_per_rank": b.passes / a.world, "fused_gates_per_rank": b.plan_gates / a.world,
             "rho_reductions_per_rank": b.reductions / a.world,
+            "deferred_tile_passes_per_rank": deferred_passes,
             "predicted_s": {"tile_passes": t_pass / a.world, "permutations": t_perm, "reductions": t_red,
-                            "exchanges": t_x, "total": t_pass / a.world + t_perm + t_red + t_x},
+                            "exchanges": t_x,
+                            "exchange_phases_overlapped": t_xphase,
+                            "exchange_phases_serial": t_xphase_serial,
+                            "total": t_pass / a.world + t_perm + t_red + t_xphase,
+                            "total_without_overlap": t_pass / a.world + t_perm + t_red + t_xphase_serial},
         }
     print(json.dumps(out, indent=1))
     if a.out:
