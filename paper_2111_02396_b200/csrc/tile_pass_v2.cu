@@ -43,6 +43,9 @@ constexpr int NBUF = 3;
 #ifndef QT_V2_ALLWAIT
 #define QT_V2_ALLWAIT 1
 #endif
+#ifndef QT_V2_PICKTREE
+#define QT_V2_PICKTREE 1
+#endif
 #ifndef QT_V2_L2PF
 #define QT_V2_L2PF 0
 #endif
@@ -346,6 +349,22 @@ __device__ __forceinline__ void rho_partial_rows3(const float2* tile, uint32_t q
 #pragma unroll
             for (int e = 0; e < 2 * D; ++e) out[2 * D * a + e] = acc[e];
     }
+}
+
+// w[i] for a warp-uniform index i (0 <= i < 32) by a branch-free select tree
+// (QT_V2_PICKTREE; the default jump table costs an indirect branch per string)
+__device__ __forceinline__ float pick_tree32(const float (&w)[32], uint32_t i) {
+    float a[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) a[k] = (i & 1u) ? w[2 * k + 1] : w[2 * k];
+    float b[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) b[k] = (i & 2u) ? a[2 * k + 1] : a[2 * k];
+    float c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c[k] = (i & 4u) ? b[2 * k + 1] : b[2 * k];
+    const float d0 = (i & 8u) ? c[1] : c[0], d1 = (i & 8u) ? c[3] : c[2];
+    return (i & 16u) ? d1 : d0;
 }
 
 struct Item {
@@ -959,7 +978,11 @@ __global__ void __launch_bounds__(kThreads, 1) tile_pass_v2_kernel(const TileArg
                                 const uint32_t zl = P.tile_mask == (uint64_t)(TILE - 1) ? (uint32_t)(ozm & (TILE - 1))
                                                                                          : to_local<T>(ozm, P);
                                 const int zs = __popcll(base & ozm) & 1;
+#if QT_V2_PICKTREE
+                                const float vv = pick_tree32(w, zl >> 8);
+#else
                                 const float vv = pick_uniform<NA>(w, (int)(zl >> 8));
+#endif
                                 const int par = (__popc((uint32_t)wtid & zl & (uint32_t)(NT - 1)) + zs) & 1;
                                 pv[j] = par ? -(double)vv : (double)vv;
                             }
